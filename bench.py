@@ -1,0 +1,428 @@
+#!/usr/bin/env python3
+"""bench.py -- S4ConvD depthwise conv1d fwd + dX + dW step on B200.
+
+Metric (BASELINE.json): effective HBM GB/s and % of the HBM roofline per path
+(fwd / dX / dW), and fwd+bwd conv time per step.
+
+* A "step" is one pass of the hot path over one batch: y = forward(x,k),
+  dx = backward_input(gy,k), dk = backward_weight(gy,x) (+ the dW combine over
+  ranks when N > 1), all through the library's C ABI on resident device
+  buffers.  Inputs come from the reference's splitmix64 stream generated in
+  place on the device.
+* Default workload: BASELINE config 3 (B=256, H=512, L=8192, K=7, fp32), the
+  largest single-GPU config and the one the north star's roofline targets are
+  stated on.  4 GiB per tensor >> 126 MB L2, so no L2 flush is needed.
+* value = algorithmic bytes of the three paths (8*B*H*L + 4*H*K each,
+  reference src/exec_model.cpp:168-179) over all ranks / device step time
+  (CUDA events, max over ranks).  Weak scaling: every rank runs the per-GPU
+  batch B, the global batch is B*N, sharded by contiguous batch rows.
+* e2e: the same metric through the host-buffer C-ABI entry points
+  (ks_dwconv1d_*_host, the reference's value-type API shape) from pinned host
+  memory, H2D/D2H inside the timed region.
+* --impl reference: the reference's own CPU conv_core.cpp (oracle/_ref, built
+  from /root/reference) on the host cores, channel-sliced over threads, on a
+  bounded channel sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {  # BASELINE.json configs, name -> (B, H, L, K)
+    "config1": (16, 64, 1024, 64),
+    "config2": (64, 128, 4096, 4096),
+    "config3": (256, 512, 8192, 7),
+    "config4": (1024, 256, 2048, 256),
+    "config5a": (512, 1024, 16384, 16),
+    "config5b": (512, 1024, 16384, 128),
+    "config5c": (512, 1024, 16384, 1024),
+}
+WORKLOAD = {
+    "config1": "reference fixture depthwise conv1d fwd+dX+dW fp32 (16,64,1024,64)",
+    "config2": "S4ConvD training-shape layer fp32 (64,128,4096,K=L=4096) fwd+bwd",
+    "config3": "short-kernel depthwise conv1d fwd+dX+dW fp32 (256,512,8192,7), bandwidth-bound",
+    "config4": "dW-dominated reduction case fp32 (1024,256,2048,256)",
+    "config5a": "S4ConvD stack sweep fp32 (512,1024,16384,16)",
+    "config5b": "S4ConvD stack sweep fp32 (512,1024,16384,128)",
+    "config5c": "S4ConvD stack sweep fp32 (512,1024,16384,1024)",
+}
+METRIC = "effective HBM GB/s & % roofline per path (fwd/dX/dW); fwd+bwd conv time/step"
+
+
+def path_bytes(B, H, L, K):
+    """Algorithmic bytes per path: read one [B,H,L] tensor + k, write one
+    [B,H,L] tensor (fwd: x,k->y; dX: gy,k->dx; dW: gy,x->dk)."""
+    return 8 * B * H * L + 4 * H * K
+
+
+def path_flops(B, H, L, K):
+    return 2 * B * H * L * K  # reference src/analyzer.cpp:36-49
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def ncu_traffic(config_name):
+    """Per-launch DRAM bytes of the dominant kernels from the committed ncu
+    --set full summary (profiles/ncu_summary.json), or None."""
+    p = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        with open(p) as f:
+            return json.load(f).get(config_name)
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for s in self.samples for n, v in zip(names, s[2:6]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle/_ref = the reference's own conv_core.cpp)
+
+def cpu_sample(cfg, threads, budget_s=12.0, mode=1, reps=1):
+    """Time fwd + dX + dW (reference default dW scheme: sequential) of the
+    reference CPU implementation on a channel sample of the workload, fanned
+    out over `threads` host threads.  Returns (GB/s, seconds, sample dict)."""
+    from oracle.oracle import SEQUENTIAL, Reference, reference_available, Oracle
+    B, H, L, K = cfg
+    impl = Reference() if reference_available() else Oracle()
+    kind = "reference" if isinstance(impl, Reference) else "port"
+
+    def run(hs):
+        o = Oracle()
+        x, k, gy = o.fill_inputs(7, B, hs, L, K)
+        t0 = time.perf_counter()
+        impl.forward(x, k, mode, threads=threads)
+        impl.backward_input(gy, k, mode, threads=threads)
+        impl.backward_weight(gy, x, K, SEQUENTIAL, 0, mode, threads=threads)
+        return time.perf_counter() - t0
+
+    hs = min(H, max(1, threads))
+    t = run(hs)
+    while t < budget_s / 4 and hs < H:  # grow the sample to a measurable size
+        hs = min(H, hs * 2)
+        t = run(hs)
+    if t < budget_s / 2 and hs < H:
+        hs = min(H, max(hs, int(hs * (budget_s / 2) / max(t, 1e-3))))
+        t = run(hs)
+    times = [t] + [run(hs) for _ in range(reps - 1)]
+    t = min(times)
+    bytes_ = 3 * path_bytes(B, hs, L, K)
+    sample = (f"{hs} of {H} channels (all B={B} rows, L={L}, K={K}), fwd+dX+dW(sequential), "
+              f"{threads} threads channel-sliced, {kind} build; full-step time extrapolated x{H / hs:.1f}")
+    return bytes_ / t / 1e9, t * H / hs, sample, kind
+
+
+def run_reference(args, cfg_name, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    B, H, L, K = cfg
+    from oracle.oracle import SEQUENTIAL, Reference, reference_available, Oracle
+    impl = Reference() if reference_available() else Oracle()
+    kind = "reference" if isinstance(impl, Reference) else "port"
+    # size the per-step channel sample so warmup+steps fit in ~2 minutes
+    _, full_s, _, _ = cpu_sample(cfg, threads, budget_s=4.0)
+    per_channel = full_s / H
+    total_steps = args.steps + args.warmup
+    hs = int(max(1, min(H, 110.0 / total_steps / max(per_channel, 1e-6))))
+    o = Oracle()
+    x, k, gy = o.fill_inputs(7, B, hs, L, K)
+    times = []
+    for i in range(total_steps):
+        t0 = time.perf_counter()
+        impl.forward(x, k, 1, threads=threads)
+        impl.backward_input(gy, k, 1, threads=threads)
+        impl.backward_weight(gy, x, K, SEQUENTIAL, 0, 1, threads=threads)
+        if i >= args.warmup:
+            times.append(time.perf_counter() - t0)
+    t = sum(times) / len(times)
+    gbs = 3 * path_bytes(B, hs, L, K) / t / 1e9
+    sample = (f"{hs} of {H} channels per step (all B={B} rows), fwd+dX+dW(sequential, Fused), "
+              f"{threads} threads channel-sliced")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * H / hs * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B": B, "H": H, "L": L,
+                   "K": K, "global_batch": B, "ms_per_step_note": "extrapolated to all H channels"},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+
+def run_ours(args, cfg_name, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2604_25422_b200 as ks
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if world == 1 and args.gpus > 1:
+            print("bench.py: --gpus N>1 must be launched under torchrun", file=sys.stderr)
+            return 2
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    B, H, L, K = cfg
+    mode = ks.FUSED if args.mode == "fused" else ks.SEPARATE
+    scheme = {"hierarchical": ks.HIERARCHICAL, "pairwise": ks.PAIRWISE}[args.scheme]
+
+    comm = None
+    if world > 1:
+        uid = [ks.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = ks.Comm(uid[0], world, rank)
+
+    # inputs: rows [rank*B, rank*B+B) of the (B*world)-row problem, generated in place
+    x, k, gy = ks.make_inputs(args.seed, B, H, L, K, device=dev, b0=rank * B, B_total=B * world)
+    y = torch.empty_like(x)
+    dx = torch.empty_like(gy)
+    dk = torch.empty((H, K), dtype=torch.float32, device=dev)
+    ws = torch.empty(max(1, ks.workspace_bytes(B, H, L, K, scheme) // 4), dtype=torch.float32,
+                     device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        ks.forward(x, k, mode, out=y)
+        if ev:
+            ev[1].record(stream)
+        ks.backward_input(gy, k, mode, out=dx)
+        if ev:
+            ev[2].record(stream)
+        ks.backward_weight(gy, x, K, scheme, 0, mode, out=dk, workspace=ws)
+        if ev:
+            ev[3].record(stream)
+        if comm is not None:
+            comm.allreduce_dw(dk)
+        if ev:
+            ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    start = torch.cuda.Event(enable_timing=True)
+    end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(stream)
+        for i in range(args.steps):
+            step(evs[i])
+        end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ms_total = start.elapsed_time(end)
+    per = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(4)] for e in evs])  # steps x 4
+    per_mean = per.mean(axis=0)
+    if world > 1:
+        t = torch.tensor([ms_total] + per_mean.tolist(), dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total, per_mean = float(t[0]), t[1:].cpu().numpy()
+    ms_step = ms_total / args.steps
+
+    pb = path_bytes(B, H, L, K)
+    value = world * 3 * pb / (ms_step * 1e-3) / 1e9
+    peak, peak_kind = measured_peaks()
+    names = ["fwd", "dX", "dW"]
+    paths = {}
+    for i, n in enumerate(names):
+        gbs = pb / (per_mean[i] * 1e-3) / 1e9
+        fl = path_flops(B, H, L, K) / (per_mean[i] * 1e-3) / 1e12
+        paths[n] = {"ms": round(float(per_mean[i]), 4), "GB_s": round(gbs, 1),
+                    "frac_hbm_measured": round(gbs / peak, 4), "frac_hbm_8TBs": round(gbs / 8000, 4),
+                    "TFLOP_s_paper": round(fl, 2)}
+    if world > 1:
+        paths["dW_allreduce"] = {"ms": round(float(per_mean[3]), 4), "bytes": 4 * H * K}
+    dom = int(np.argmax(per_mean[:3]))
+    traffic = ncu_traffic(cfg_name)
+    dom_traffic = None
+    if traffic and names[dom] in traffic:
+        dom_traffic = traffic[names[dom]].get("dram_bytes")
+    achieved = pb / (per_mean[dom] * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": dom_traffic,
+                "kernel": names[dom], "peak_kind": peak_kind,
+                "algorithmic_bytes_per_launch": pb,
+                "note": "achieved = (8*B*H*L + 4*H*K) bytes / mean CUDA-event duration of the path"}
+    launches_per_step = 2 + (2 if scheme == ks.HIERARCHICAL else 1)
+
+    # ---- end to end through the host-buffer C ABI (pinned host memory) ----
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.empty((B, H, L), dtype=torch.float32, pin_memory=True)
+        gyh = torch.empty_like(xh, pin_memory=True)
+        yh = torch.empty_like(xh, pin_memory=True)
+        dxh = torch.empty_like(xh, pin_memory=True)
+        kh = torch.empty((H, K), dtype=torch.float32, pin_memory=True)
+        dkh = torch.empty((H, K), dtype=torch.float32, pin_memory=True)
+        xh.copy_(x)
+        gyh.copy_(gy)
+        kh.copy_(k)
+        xn, gyn, yn, dxn, kn, dkn = (t.numpy() for t in (xh, gyh, yh, dxh, kh, dkh))
+        del y, dx
+        torch.cuda.empty_cache()
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+
+        def host_step():
+            ks.forward(xn, kn, mode, out=yn)
+            ks.backward_input(gyn, kn, mode, out=dxn)
+            ks.backward_weight(gyn, xn, K, scheme, 0, mode, out=dkn)
+
+        host_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            host_step()
+        t_host = (time.perf_counter() - t0) / e2e_steps
+        if world > 1:
+            tt = torch.tensor([t_host], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_host = float(tt[0])
+        tb = 4 * B * H * L
+        e2e = {"value": round(world * 3 * pb / t_host / 1e9, 2), "unit": "GB/s",
+               "h2d_bytes_per_step": 4 * tb + 2 * 4 * H * K, "d2h_bytes_per_step": 2 * tb + 4 * H * K,
+               "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps,
+               "path": "ks_dwconv1d_{fwd,dx,dw}_f32_host, pinned host buffers, wall clock"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        gbs, _, sample, kind = cpu_sample(cfg, threads)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
+               "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (reference splitmix64 stream, generated on device)",
+            "config": {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B_per_gpu": B, "H": H,
+                       "L": L, "K": K, "global_batch": B * world,
+                       "parallelism": f"batch-shard dp{world}" + (" + NCCL dW allreduce" if world > 1 else ""),
+                       "mode": args.mode, "dw_scheme": args.scheme,
+                       "l2": "inputs larger than L2 (no flush)" if 4 * B * H * L > 2 * 126e6
+                             else "working set fits L2 (not flushed)"},
+            "paths": paths, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps,
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if comm is not None:
+        comm.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="config3")
+    ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
+    ap.add_argument("--scheme", choices=["hierarchical", "pairwise"], default="hierarchical")
+    ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, args.config, cfg)
+    return run_ours(args, args.config, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

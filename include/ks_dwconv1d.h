@@ -1,0 +1,163 @@
+/*
+ * ks_dwconv1d.h -- C ABI of the B200-native S4ConvD depthwise conv1d operator.
+ *
+ * This is the drop-in boundary for the reference's hot path, the three
+ * operator entry points of kernelscope::conv
+ * (/root/reference/proj/include/kernelscope/conv_core.hpp:49-69):
+ *
+ *   reference (C++, host value types)             C ABI here (device pointers)
+ *   conv::forward(x,k,shape,mode)        :49-52   ks_dwconv1d_fwd_f32 / _f64
+ *   conv::backward_input(gy,k,shape,mode):56-59   ks_dwconv1d_dx_f32  / _f64
+ *   conv::backward_weight(gy,x,shape,
+ *                         scheme,mode)   :64-69   ks_dwconv1d_dw_f32  / _f64
+ *
+ * plus host-buffer twins (*_host) that take plain host pointers, which is the
+ * shape of the reference's value-type API, and the batch-sharded multi-GPU
+ * combine for dW.  The C++ drop-in (include/kernelscope/conv_core.hpp, same
+ * names and signatures as the reference) is a thin layer over these calls.
+ *
+ * Conventions
+ *  - Layout: x, y, gy, dx are row-major [B,H,L] (element (b,h,t) at
+ *    (b*H+h)*L+t, reference tensor.hpp:15-32); k and dk are row-major [H,K]
+ *    (tensor.hpp:45-69).  Padding p = K/2 (shape.hpp:16); dX uses q = K-1-p
+ *    (src/conv_core.cpp:56).
+ *  - Device entry points take device pointers, are asynchronous on `stream`
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream) and never
+ *    synchronise.  No exceptions cross the boundary; every call returns a
+ *    ks_status.
+ *  - Determinism: for fixed (shape, mode, scheme) results are bitwise
+ *    reproducible run to run; there are no floating-point atomics anywhere.
+ *  - Rounding: y and dX accumulate taps in ascending j from +0, exactly like
+ *    the reference loops (src/conv_core.cpp:37-40, 66-69), so they are
+ *    bit-identical to the reference in both MulAddModes.  dW schemes
+ *    SEQUENTIAL / PAIRWISE / CHUNKED reproduce the reference association order
+ *    bit-for-bit (src/conv_core.cpp:98-146); HIERARCHICAL is this library's
+ *    fast deterministic order (parity within a stated tolerance).
+ */
+#ifndef KS_DWCONV1D_H
+#define KS_DWCONV1D_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KS_DWCONV1D_ABI_VERSION 1
+
+typedef enum ks_status {
+    KS_OK = 0,
+    KS_ERR_DIM_B = 1,      /* B < 1                         (shape.hpp:27)          */
+    KS_ERR_DIM_H = 2,      /* H < 1                         (shape.hpp:28)          */
+    KS_ERR_DIM_L = 3,      /* L < 1                         (shape.hpp:29)          */
+    KS_ERR_DIM_K = 4,      /* K < 1                         (shape.hpp:30)          */
+    KS_ERR_BAD_CHUNK = 5,  /* chunked scheme, chunk < 1     (src/conv_core.cpp:154) */
+    KS_ERR_BAD_MODE = 6,   /* mode not a ks_muladd                                  */
+    KS_ERR_BAD_SCHEME = 7, /* scheme not a ks_dw_scheme                             */
+    KS_ERR_NULL = 8,       /* a required pointer is NULL                             */
+    KS_ERR_WORKSPACE = 9,  /* ws_bytes smaller than ks_dwconv1d_dw_workspace_bytes   */
+    KS_ERR_NO_DEVICE = 10, /* no CUDA device / driver                                */
+    KS_ERR_CUDA = 11,      /* CUDA runtime error (ks_last_error_string for text)     */
+    KS_ERR_NCCL = 12,      /* NCCL error                                             */
+    KS_ERR_SHARD = 13      /* bad rank / world size / shard geometry                 */
+} ks_status;
+
+/* MulAddMode (conv_core.hpp:45): SEPARATE = acc + a*b with two roundings (the
+ * reference default), FUSED = fma(a,b,acc). */
+typedef enum ks_muladd { KS_MULADD_SEPARATE = 0, KS_MULADD_FUSED = 1 } ks_muladd;
+
+/* dW association order.  The first three are the reference's SumScheme
+ * (conv_core.hpp:14-18) and are reproduced bit-for-bit; HIERARCHICAL is the
+ * fast path (in-register FMA partials over t, shared-memory tree, fixed-order
+ * cross-block pass; no atomics). */
+typedef enum ks_dw_scheme {
+    KS_DW_SEQUENTIAL = 0,
+    KS_DW_PAIRWISE = 1,
+    KS_DW_CHUNKED = 2,
+    KS_DW_HIERARCHICAL = 3
+} ks_dw_scheme;
+
+const char* ks_status_string(ks_status s);
+/* Text of the last CUDA/NCCL error seen by this thread ("" if none). */
+const char* ks_last_error_string(void);
+int ks_abi_version(void);
+
+/* ---- device-pointer entry points (asynchronous on `stream`) -------------- */
+
+ks_status ks_dwconv1d_fwd_f32(const float* x, const float* k, float* y, int64_t B, int64_t H,
+                              int64_t L, int64_t K, int mode, void* stream);
+ks_status ks_dwconv1d_fwd_f64(const double* x, const double* k, double* y, int64_t B,
+                              int64_t H, int64_t L, int64_t K, int mode, void* stream);
+
+ks_status ks_dwconv1d_dx_f32(const float* gy, const float* k, float* dx, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int mode, void* stream);
+ks_status ks_dwconv1d_dx_f64(const double* gy, const double* k, double* dx, int64_t B,
+                             int64_t H, int64_t L, int64_t K, int mode, void* stream);
+
+/* Scratch bytes ks_dwconv1d_dw_* needs for this shape/scheme (may be 0). */
+ks_status ks_dwconv1d_dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K,
+                                         int scheme, int64_t chunk, int elem_bytes,
+                                         size_t* bytes);
+/* ws may be NULL (then the library takes stream-ordered scratch itself);
+ * otherwise ws_bytes must be >= ks_dwconv1d_dw_workspace_bytes(...).
+ * `chunk` is only read for KS_DW_CHUNKED (chunk >= B*L degenerates to
+ * SEQUENTIAL, src/conv_core.cpp:172-174); `mode` is ignored by PAIRWISE, whose
+ * leaves are plain products (src/conv_core.cpp:88-95). */
+ks_status ks_dwconv1d_dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int scheme, int64_t chunk, int mode,
+                             void* ws, size_t ws_bytes, void* stream);
+ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int64_t B,
+                             int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                             int mode, void* ws, size_t ws_bytes, void* stream);
+
+/* On-device splitmix64 generator, bit-identical to the reference's
+ * SplitMix64::next_pm1 (include/kernelscope/rng.hpp:12-28): out[i] = draw
+ * (first+1+i) of the stream seeded with `seed`.  validate() draws x, then k,
+ * then gy (src/conv_core.cpp:241-247), so x = fill(seed,0), k =
+ * fill(seed,B*H*L), gy = fill(seed,B*H*L+H*K). */
+ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream);
+
+/* ---- host-buffer entry points (synchronous; the value-type API shape) ---- */
+/* Inputs/outputs are host pointers (pinned or pageable).  The call streams
+ * row blocks host->device, runs the kernels and streams results back with
+ * copy/compute overlap on the current device, then returns. */
+ks_status ks_dwconv1d_fwd_f32_host(const float* x, const float* k, float* y, int64_t B,
+                                   int64_t H, int64_t L, int64_t K, int mode);
+ks_status ks_dwconv1d_dx_f32_host(const float* gy, const float* k, float* dx, int64_t B,
+                                  int64_t H, int64_t L, int64_t K, int mode);
+ks_status ks_dwconv1d_dw_f32_host(const float* gy, const float* x, float* dk, int64_t B,
+                                  int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                                  int mode);
+ks_status ks_dwconv1d_fwd_f64_host(const double* x, const double* k, double* y, int64_t B,
+                                   int64_t H, int64_t L, int64_t K, int mode);
+ks_status ks_dwconv1d_dx_f64_host(const double* gy, const double* k, double* dx, int64_t B,
+                                  int64_t H, int64_t L, int64_t K, int mode);
+ks_status ks_dwconv1d_dw_f64_host(const double* gy, const double* x, double* dk, int64_t B,
+                                  int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                                  int mode);
+
+/* ---- batch sharding across GPUs (one process per GPU) --------------------- */
+/* Contiguous batch slice of rank `rank` out of `world`: rows [*b0, *b0+*nb).
+ * Slices differ by at most one row; pure host arithmetic (no device). */
+ks_status ks_shard_rows(int64_t B, int world, int rank, int64_t* b0, int64_t* nb);
+
+typedef struct ks_comm ks_comm;
+/* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
+ks_status ks_comm_unique_id(void* id128);
+ks_status ks_comm_init(ks_comm** comm, const void* id128, int world, int rank);
+ks_status ks_comm_destroy(ks_comm* comm);
+/* In-place sum of the rank-local dk[H,K] over all ranks: one ncclAllReduce on
+ * `stream`. */
+ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm* comm,
+                                       void* stream);
+/* Deterministic, world-size-invariant combine: all-gathers the per-rank
+ * dk[H,K] into gather[world,H,K] (device scratch) and sums it in rank order
+ * with a fixed pairwise tree, so every rank ends with the same bits. */
+ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, int64_t K,
+                                           ks_comm* comm, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KS_DWCONV1D_H */

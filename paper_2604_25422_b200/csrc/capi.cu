@@ -1,0 +1,222 @@
+// capi.cu -- the extern "C" device-pointer entry points of include/ks_dwconv1d.h:
+// argument validation in the reference's order (ConvShape ctor checks B,H,L,K,
+// shape.hpp:27-31; chunk_size >= 1, src/conv_core.cpp:154-156), launch
+// selection, scratch management and the on-device splitmix64 generator.
+#include <cstring>
+#include <string>
+
+#include "ks_common.cuh"
+
+namespace ks {
+
+ks_status conv_stencil_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t,
+                           int64_t, int, int, cudaStream_t);
+ks_status conv_stencil_f64(const double*, const double*, double*, int64_t, int64_t, int64_t,
+                           int64_t, int64_t, int, int, cudaStream_t);
+size_t dw_workspace_bytes(int64_t, int64_t, int64_t, int64_t, int, int64_t, int);
+ks_status dw_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int,
+                 int64_t, int, void*, cudaStream_t);
+ks_status dw_f64(const double*, const double*, double*, int64_t, int64_t, int64_t, int64_t, int,
+                 int64_t, int, void*, cudaStream_t);
+
+static thread_local std::string g_last_error;
+
+void set_last_error(const char* what) { g_last_error = what ? what : ""; }
+
+ks_status cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return KS_OK;
+    g_last_error = cudaGetErrorString(e);
+    if (e == cudaErrorNoDevice || e == cudaErrorInsufficientDriver) return KS_ERR_NO_DEVICE;
+    return KS_ERR_CUDA;
+}
+
+ks_status check_launch() { return cuda_status(cudaGetLastError()); }
+
+static ks_status check_shape(int64_t B, int64_t H, int64_t L, int64_t K) {
+    if (B < 1) return KS_ERR_DIM_B;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (L < 1) return KS_ERR_DIM_L;
+    if (K < 1) return KS_ERR_DIM_K;
+    return KS_OK;
+}
+
+static ks_status check_mode(int mode) {
+    return (mode == KS_MULADD_SEPARATE || mode == KS_MULADD_FUSED) ? KS_OK : KS_ERR_BAD_MODE;
+}
+
+static ks_status check_dw(int scheme, int64_t chunk) {
+    if (scheme < KS_DW_SEQUENTIAL || scheme > KS_DW_HIERARCHICAL) return KS_ERR_BAD_SCHEME;
+    if (scheme == KS_DW_CHUNKED && chunk < 1) return KS_ERR_BAD_CHUNK;
+    return KS_OK;
+}
+
+// Fails loudly when there is no usable device: this library has no CPU path.
+static ks_status check_device() {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        g_last_error = e != cudaSuccess ? cudaGetErrorString(e) : "no CUDA device";
+        return KS_ERR_NO_DEVICE;
+    }
+    return KS_OK;
+}
+
+#define KS_TRY(expr)                        \
+    do {                                    \
+        const ks_status _s = (expr);        \
+        if (_s != KS_OK) return _s;         \
+    } while (0)
+
+// splitmix64 draw n (1-based) of SplitMix64(seed) mapped like next_pm1()
+// (include/kernelscope/rng.hpp:17-28).  The 2u-1 step is done in double with
+// explicit round-to-nearest intrinsics, then rounded to float once.
+__global__ void fill_pm1_kernel(uint64_t seed, uint64_t first, float* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + (first + 1 + static_cast<uint64_t>(i)) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z = z ^ (z >> 31);
+        const double unit = __dmul_rn(static_cast<double>(z >> 11), 0x1.0p-53);
+        out[i] = __double2float_rn(__dadd_rn(__dmul_rn(2.0, unit), -1.0));
+    }
+}
+
+// Scratch for dW: caller-provided, or stream-ordered from the device pool.
+struct Scratch {
+    void* ptr = nullptr;
+    bool owned = false;
+    cudaStream_t st = nullptr;
+    ks_status take(void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
+        st = s;
+        if (need == 0) return KS_OK;
+        if (ws) {
+            if (ws_bytes < need) return KS_ERR_WORKSPACE;
+            ptr = ws;
+            return KS_OK;
+        }
+        owned = true;
+        return cuda_status(cudaMallocAsync(&ptr, need, s));
+    }
+    ~Scratch() {
+        if (owned && ptr) cudaFreeAsync(ptr, st);
+    }
+};
+
+}  // namespace ks
+
+using namespace ks;
+
+extern "C" {
+
+const char* ks_status_string(ks_status s) {
+    switch (s) {
+        case KS_OK: return "ok";
+        case KS_ERR_DIM_B: return "axis B must be >= 1";
+        case KS_ERR_DIM_H: return "axis H must be >= 1";
+        case KS_ERR_DIM_L: return "axis L must be >= 1";
+        case KS_ERR_DIM_K: return "axis K must be >= 1";
+        case KS_ERR_BAD_CHUNK: return "chunk_size must be >= 1";
+        case KS_ERR_BAD_MODE: return "unknown MulAddMode";
+        case KS_ERR_BAD_SCHEME: return "unknown accumulation scheme";
+        case KS_ERR_NULL: return "null pointer argument";
+        case KS_ERR_WORKSPACE: return "workspace too small";
+        case KS_ERR_NO_DEVICE: return "no CUDA device";
+        case KS_ERR_CUDA: return "CUDA error";
+        case KS_ERR_NCCL: return "NCCL error";
+        case KS_ERR_SHARD: return "bad shard geometry";
+    }
+    return "unknown status";
+}
+
+const char* ks_last_error_string(void) { return g_last_error.c_str(); }
+int ks_abi_version(void) { return KS_DWCONV1D_ABI_VERSION; }
+
+ks_status ks_dwconv1d_fwd_f32(const float* x, const float* k, float* y, int64_t B, int64_t H,
+                              int64_t L, int64_t K, int mode, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (!x || !k || !y) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    return conv_stencil_f32(x, k, y, B, H, L, K, K / 2, 0, mode, static_cast<cudaStream_t>(stream));
+}
+
+ks_status ks_dwconv1d_fwd_f64(const double* x, const double* k, double* y, int64_t B, int64_t H,
+                              int64_t L, int64_t K, int mode, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (!x || !k || !y) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    return conv_stencil_f64(x, k, y, B, H, L, K, K / 2, 0, mode, static_cast<cudaStream_t>(stream));
+}
+
+ks_status ks_dwconv1d_dx_f32(const float* gy, const float* k, float* dx, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int mode, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (!gy || !k || !dx) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    return conv_stencil_f32(gy, k, dx, B, H, L, K, K - 1 - K / 2, 1, mode,
+                            static_cast<cudaStream_t>(stream));
+}
+
+ks_status ks_dwconv1d_dx_f64(const double* gy, const double* k, double* dx, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int mode, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (!gy || !k || !dx) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    return conv_stencil_f64(gy, k, dx, B, H, L, K, K - 1 - K / 2, 1, mode,
+                            static_cast<cudaStream_t>(stream));
+}
+
+ks_status ks_dwconv1d_dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme,
+                                         int64_t chunk, int elem_bytes, size_t* bytes) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_dw(scheme, chunk));
+    if (!bytes) return KS_ERR_NULL;
+    if (elem_bytes != 4 && elem_bytes != 8) return KS_ERR_BAD_MODE;
+    *bytes = dw_workspace_bytes(B, H, L, K, scheme, chunk, elem_bytes);
+    return KS_OK;
+}
+
+ks_status ks_dwconv1d_dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int scheme, int64_t chunk, int mode, void* ws,
+                             size_t ws_bytes, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_dw(scheme, chunk));
+    KS_TRY(check_mode(mode));
+    if (!gy || !x || !dk) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch s;
+    KS_TRY(s.take(ws, ws_bytes, dw_workspace_bytes(B, H, L, K, scheme, chunk, 4), st));
+    return dw_f32(gy, x, dk, B, H, L, K, scheme, chunk, mode, s.ptr, st);
+}
+
+ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int64_t B, int64_t H,
+                             int64_t L, int64_t K, int scheme, int64_t chunk, int mode, void* ws,
+                             size_t ws_bytes, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_dw(scheme, chunk));
+    KS_TRY(check_mode(mode));
+    if (!gy || !x || !dk) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch s;
+    KS_TRY(s.take(ws, ws_bytes, dw_workspace_bytes(B, H, L, K, scheme, chunk, 8), st));
+    return dw_f64(gy, x, dk, B, H, L, K, scheme, chunk, mode, s.ptr, st);
+}
+
+ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream) {
+    if (n < 0) return KS_ERR_DIM_L;
+    if (n == 0) return KS_OK;
+    if (!out) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    const int64_t want = (n + 255) / 256;
+    const unsigned blocks = static_cast<unsigned>(want < int64_t(num_sms()) * 64 ? want : int64_t(num_sms()) * 64);
+    fill_pm1_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first, out, n);
+    return check_launch();
+}
+
+}  // extern "C"

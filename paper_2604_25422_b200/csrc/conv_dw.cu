@@ -1,0 +1,489 @@
+// conv_dw.cu -- weight-gradient dW kernels (sm_100a).
+//
+//   dk[h,j] = sum_b sum_t gy[b,h,t] * x[b,h,t+j-p]      (src/conv_core.cpp:148-181)
+//
+// The association order of that B*L-deep sum is the whole story of dW:
+//
+//  * HIERARCHICAL (fast path): in-register FMA partials over t for an 8-tap
+//    register block, a fixed warp-shuffle tree, a fixed shared-memory pass over
+//    warps, per-CTA partials [G,H,K] in global scratch, then a fixed-order
+//    cross-block pass.  Deterministic, no atomics; parity by tolerance.
+//  * PAIRWISE: the reference's midpoint tree over the flat index
+//    (src/conv_core.cpp:113-118), evaluated bit-exactly: the top 8 tree levels
+//    in shared memory, each depth-8 subtree by one thread.
+//  * CHUNKED / SEQUENTIAL: per-chunk sequential chains then `total += partial`
+//    in chunk order (src/conv_core.cpp:98-146), bit-exactly.
+#include <algorithm>
+
+#include "ks_common.cuh"
+
+namespace ks {
+
+// ---------------------------------------------------------------------------
+// HIERARCHICAL
+//
+// CTA = (row group g, channel h, tap tile jt).  256 threads = NJ tap groups of
+// JR=8 taps x NTS = 256/NJ t-slices.  Per (row, 2048-wide t tile) the CTA stages
+// gy[t0, t0+TT) and x[t0+j0-p-S, ...) in padded shared memory; thread (jg,ts)
+// walks 8-wide t blocks interleaved across the t-slices (lane stride 8 floats,
+// conflict-free float4 reads) and does 8x8 FMAs per block from registers.
+constexpr int kDwThreads = 256;
+constexpr int kDwTT = 2048;  // t per staged tile
+constexpr int kJR = 8;       // taps per thread
+constexpr int kTB = 8;       // t per register block
+
+template <int NJ, int S>
+struct DwGeom {
+    static constexpr int NTS = kDwThreads / NJ;
+    static constexpr int JT = NJ * kJR;
+    static constexpr int SPT = kDwTT / (NTS * kTB);  // register blocks per tile per thread
+    static constexpr int NVX = (S + kTB + kJR - 1 + 3) / 4;
+    static constexpr int XL = kDwTT + JT + 8;  // staged x window (logical floats, %4 == 0)
+    static constexpr int GY_FLOATS = padded_len(kDwTT);
+    static constexpr int X_FLOATS = padded_len(XL);
+};
+
+template <int NJ, int S, bool FUSED>
+__global__ void __launch_bounds__(kDwThreads)
+dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
+               float* __restrict__ part, int B, int H, int L, int K, int p, int G, int NJT) {
+    using Geo = DwGeom<NJ, S>;
+    __shared__ __align__(16) float gys[Geo::GY_FLOATS];
+    __shared__ __align__(16) float xs[Geo::X_FLOATS];
+    __shared__ float red[kDwThreads / 32][kJR];
+
+    int bid = blockIdx.x;
+    const int jt = bid % NJT;
+    bid /= NJT;
+    const int h = bid % H;
+    const int g = bid / H;
+    const int b_begin = static_cast<int>(static_cast<int64_t>(B) * g / G);
+    const int b_end = static_cast<int>(static_cast<int64_t>(B) * (g + 1) / G);
+    const int j0 = jt * Geo::JT;
+    const int tid = threadIdx.x;
+    const int jg = tid / Geo::NTS;
+    const int ts = tid - jg * Geo::NTS;
+    const bool vec_ok = (L & 3) == 0;
+
+    float acc[kJR];
+#pragma unroll
+    for (int i = 0; i < kJR; ++i) acc[i] = 0.f;
+
+    for (int b = b_begin; b < b_end; ++b) {
+        const int64_t row = static_cast<int64_t>(b) * H + h;
+        const float* rg = gy + row * L;
+        const float* rx = x + row * L;
+        for (int t0 = 0; t0 < L; t0 += kDwTT) {
+            // stage gy tile
+            for (int c = tid; c < kDwTT / 4; c += kDwThreads) {
+                const int q = t0 + 4 * c;
+                float4 v;
+                if (vec_ok && q + 3 < L) {
+                    v = ld_nc_v4(rg + q);
+                } else {
+                    v.x = q + 0 < L ? rg[q + 0] : 0.f;
+                    v.y = q + 1 < L ? rg[q + 1] : 0.f;
+                    v.z = q + 2 < L ? rg[q + 2] : 0.f;
+                    v.w = q + 3 < L ? rg[q + 3] : 0.f;
+                }
+                *reinterpret_cast<float4*>(gys + pad_idx(4 * c)) = v;
+            }
+            // stage x window, logical index i <-> x position a0 + i
+            const int a0 = t0 + j0 - p - S;
+            for (int c = tid; c < Geo::XL / 4; c += kDwThreads) {
+                const int q = a0 + 4 * c;
+                float4 v;
+                if (vec_ok && q >= 0 && q + 3 < L) {
+                    v = ld_nc_v4(rx + q);
+                } else {
+                    v.x = (q + 0 >= 0 && q + 0 < L) ? rx[q + 0] : 0.f;
+                    v.y = (q + 1 >= 0 && q + 1 < L) ? rx[q + 1] : 0.f;
+                    v.z = (q + 2 >= 0 && q + 2 < L) ? rx[q + 2] : 0.f;
+                    v.w = (q + 3 >= 0 && q + 3 < L) ? rx[q + 3] : 0.f;
+                }
+                *reinterpret_cast<float4*>(xs + pad_idx(4 * c)) = v;
+            }
+            __syncthreads();
+#pragma unroll 2
+            for (int s = 0; s < Geo::SPT; ++s) {
+                const int tl = (s * Geo::NTS + ts) * kTB;
+                if (t0 + tl < L) {
+                    float gv[kTB];
+#pragma unroll
+                    for (int c = 0; c < kTB / 4; ++c) {
+                        const float4 q = *reinterpret_cast<const float4*>(gys + pad_idx(tl + 4 * c));
+                        gv[4 * c + 0] = q.x;
+                        gv[4 * c + 1] = q.y;
+                        gv[4 * c + 2] = q.z;
+                        gv[4 * c + 3] = q.w;
+                    }
+                    float xv[4 * Geo::NVX];
+#pragma unroll
+                    for (int c = 0; c < Geo::NVX; ++c) {
+                        const float4 q = *reinterpret_cast<const float4*>(
+                            xs + pad_idx(tl + jg * kJR + 4 * c));
+                        xv[4 * c + 0] = q.x;
+                        xv[4 * c + 1] = q.y;
+                        xv[4 * c + 2] = q.z;
+                        xv[4 * c + 3] = q.w;
+                    }
+#pragma unroll
+                    for (int tt = 0; tt < kTB; ++tt)
+#pragma unroll
+                        for (int jj = 0; jj < kJR; ++jj)
+                            acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+                }
+            }
+            __syncthreads();
+        }
+    }
+
+    // fixed-order reduction over the t-slices of each tap group
+#pragma unroll
+    for (int jj = 0; jj < kJR; ++jj) {
+        float v = acc[jj];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc[jj] = v;
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) {
+#pragma unroll
+        for (int jj = 0; jj < kJR; ++jj) red[warp][jj] = acc[jj];
+    }
+    __syncthreads();
+    constexpr int WPG = Geo::NTS / 32;  // warps per tap group
+    if (tid < Geo::JT) {
+        const int gj = tid / kJR, jj = tid % kJR;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < WPG; ++w) s += red[gj * WPG + w][jj];
+        const int j = j0 + tid;
+        if (j < K) part[(static_cast<int64_t>(g) * H + h) * K + j] = s;
+    }
+}
+
+// dk[h,j] = fixed-order sum over the G row-group partials.
+template <typename T>
+__global__ void dw_sum_groups(const T* __restrict__ part, T* __restrict__ dk, int64_t HK, int G) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= HK) return;
+    T s = part[i];
+    for (int g = 1; g < G; ++g) s += part[static_cast<int64_t>(g) * HK + i];
+    dk[i] = s;
+}
+
+// ---------------------------------------------------------------------------
+// PAIRWISE (exact)
+
+template <typename T>
+__device__ __forceinline__ T dw_leaf(const T* __restrict__ gy, const T* __restrict__ x,
+                                     int64_t H, int64_t h, int64_t d, int64_t L, int64_t flat) {
+    // WeightTerm::operator() (src/conv_core.cpp:88-95): plain product or +0.
+    const int64_t b = flat / L;
+    const int64_t t = flat - b * L;
+    const int64_t xi = t + d;
+    if (xi < 0 || xi >= L) return T(0);
+    const int64_t row = (b * H + h) * L;
+    if constexpr (sizeof(T) == 4) return __fmul_rn(gy[row + t], x[row + xi]);
+    else return __dmul_rn(gy[row + t], x[row + xi]);
+}
+
+// Midpoint-split recursion of reduce_pairwise, restated iteratively with an
+// explicit stack so deep subtrees need no device call stack.
+template <typename T>
+__device__ T dw_pairwise_subtree(const T* __restrict__ gy, const T* __restrict__ x, int64_t H,
+                                 int64_t h, int64_t d, int64_t L, int64_t lo, int64_t hi) {
+    // Post-order walk: each frame is [lo,hi) with a flag telling whether its
+    // left child's value has been pushed.
+    int64_t st_lo[48], st_hi[48];
+    T vals[48];
+    int st_state[48];
+    int sp = 0, vp = 0;
+    st_lo[0] = lo;
+    st_hi[0] = hi;
+    st_state[0] = 0;
+    sp = 1;
+    while (sp > 0) {
+        const int top = sp - 1;
+        const int64_t a = st_lo[top], c = st_hi[top];
+        if (c - a == 1) {
+            vals[vp++] = dw_leaf<T>(gy, x, H, h, d, L, a);
+            --sp;
+            continue;
+        }
+        const int64_t mid = a + (c - a) / 2;
+        if (st_state[top] == 0) {
+            st_state[top] = 1;
+            st_lo[sp] = a;
+            st_hi[sp] = mid;
+            st_state[sp] = 0;
+            ++sp;
+        } else if (st_state[top] == 1) {
+            st_state[top] = 2;
+            st_lo[sp] = mid;
+            st_hi[sp] = c;
+            st_state[sp] = 0;
+            ++sp;
+        } else {
+            const T right = vals[--vp];
+            const T left = vals[--vp];
+            vals[vp++] = left + right;
+            --sp;
+        }
+    }
+    return vals[0];
+}
+
+// One CTA per (h,j).  Depth-D nodes (D <= 8) each computed by one thread; all
+// nodes above depth D are internal (size >= 2), so the top is a perfect binary
+// tree combined in shared memory with children (2i, 2i+1).
+template <typename T>
+__global__ void __launch_bounds__(256)
+dw_pairwise_exact(const T* __restrict__ gy, const T* __restrict__ x, T* __restrict__ dk,
+                  int64_t B, int64_t H, int64_t L, int64_t K, int D) {
+    __shared__ T buf[2][256];
+    const int64_t hj = blockIdx.x;
+    const int64_t h = hj / K, j = hj - h * K;
+    const int64_t d = j - K / 2;
+    const int64_t n = B * L;
+    const int nn = 1 << D;
+    const int i = threadIdx.x;
+    if (i < nn) {
+        int64_t lo = 0, hi = n;
+        for (int lev = D - 1; lev >= 0; --lev) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if ((i >> lev) & 1) lo = mid;
+            else hi = mid;
+        }
+        buf[0][i] = dw_pairwise_subtree<T>(gy, x, H, h, d, L, lo, hi);
+    }
+    __syncthreads();
+    int src = 0;
+    for (int w = nn >> 1; w >= 1; w >>= 1) {
+        if (i < w) buf[src ^ 1][i] = buf[src][2 * i] + buf[src][2 * i + 1];
+        __syncthreads();
+        src ^= 1;
+    }
+    if (i == 0) dk[hj] = buf[src][0];
+}
+
+// ---------------------------------------------------------------------------
+// CHUNKED / SEQUENTIAL (exact)
+
+// Sequential chain over the valid flat indices of [f_lo, f_hi) for tap offset d
+// (the inner loops of reduce_sequential / reduce_chunked).
+template <typename T, bool FUSED>
+__device__ T dw_chain(const T* __restrict__ gy, const T* __restrict__ x, int64_t H, int64_t h,
+                      int64_t d, int64_t L, int64_t f_lo, int64_t f_hi) {
+    const int64_t t_lo = d < 0 ? -d : 0;
+    const int64_t t_hi = d > 0 ? L - d : L;
+    T acc = T(0);
+    int64_t b = f_lo / L;
+    for (int64_t f = b * L; f < f_hi; f += L, ++b) {
+        const int64_t row = (b * H + h) * L;
+        int64_t ta = f_lo > f ? f_lo - f : 0;
+        int64_t tb = f_hi - f < L ? f_hi - f : L;
+        if (ta < t_lo) ta = t_lo;
+        if (tb > t_hi) tb = t_hi;
+        for (int64_t t = ta; t < tb; ++t) acc = muladd<FUSED>(acc, gy[row + t], x[row + t + d]);
+    }
+    return acc;
+}
+
+// part[c,h,j] = chain over chunk c.  Threads of a warp take consecutive taps of
+// one (h, chunk), so gy reads broadcast and x reads coalesce.
+template <typename T, bool FUSED>
+__global__ void __launch_bounds__(256)
+dw_chunk_partials(const T* __restrict__ gy, const T* __restrict__ x, T* __restrict__ part,
+                  int64_t B, int64_t H, int64_t L, int64_t K, int64_t chunk, int64_t nchunks) {
+    const int64_t total = nchunks * H * K;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t j = i % K;
+        const int64_t ch = i / K;  // c*H + h
+        const int64_t h = ch % H;
+        const int64_t c = ch / H;
+        const int64_t f_lo = c * chunk;
+        const int64_t f_hi = std::min<int64_t>(f_lo + chunk, B * L);
+        part[i] = dw_chain<T, FUSED>(gy, x, H, h, j - K / 2, L, f_lo, f_hi);
+    }
+}
+
+// dk = ((0 + part[0]) + part[1]) + ... in chunk order (reduce_chunked's
+// `total += partial`, :135-145).  With one chunk (SEQUENTIAL or chunk >= B*L)
+// the chain is returned as is (reduce_sequential).
+template <typename T>
+__global__ void dw_chunk_total(const T* __restrict__ part, T* __restrict__ dk, int64_t HK,
+                               int64_t nchunks) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= HK) return;
+    if (nchunks == 1) {
+        dk[i] = part[i];
+        return;
+    }
+    T total = T(0);
+    for (int64_t c = 0; c < nchunks; ++c) total = total + part[c * HK + i];
+    dk[i] = total;
+}
+
+// Workspace-free variant for huge chunk counts: one thread per (h,j) walks its
+// chunks in order.
+template <typename T, bool FUSED>
+__global__ void dw_chunked_fused(const T* __restrict__ gy, const T* __restrict__ x,
+                                 T* __restrict__ dk, int64_t B, int64_t H, int64_t L, int64_t K,
+                                 int64_t chunk, int64_t nchunks) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= H * K) return;
+    const int64_t h = i / K, j = i - h * K;
+    T total = T(0);
+    for (int64_t c = 0; c < nchunks; ++c) {
+        const int64_t f_lo = c * chunk;
+        const int64_t f_hi = std::min<int64_t>(f_lo + chunk, B * L);
+        total = total + dw_chain<T, FUSED>(gy, x, H, h, j - K / 2, L, f_lo, f_hi);
+    }
+    dk[i] = total;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+
+namespace {
+
+struct HierPlan {
+    int nj;   // tap groups per CTA (1,2,4,8)
+    int njt;  // tap tiles
+    int g;    // row groups
+};
+
+HierPlan hier_plan(int64_t B, int64_t H, int64_t K) {
+    HierPlan pl;
+    const int64_t groups8 = (K + kJR - 1) / kJR;
+    pl.nj = 1;
+    while (pl.nj < 8 && pl.nj < groups8) pl.nj *= 2;
+    pl.njt = static_cast<int>((K + pl.nj * kJR - 1) / (pl.nj * kJR));
+    const int64_t target = 8192;
+    int64_t g = (target + H * pl.njt - 1) / (H * pl.njt);
+    g = std::max<int64_t>(1, std::min<int64_t>(g, B));
+    pl.g = static_cast<int>(g);
+    return pl;
+}
+
+constexpr size_t kChunkWsCap = size_t(512) << 20;
+
+int64_t chunk_count(int64_t B, int64_t L, int scheme, int64_t chunk) {
+    const int64_t n = B * L;
+    if (scheme == KS_DW_SEQUENTIAL || chunk >= n) return 1;
+    return (n + chunk - 1) / chunk;
+}
+
+template <int NJ, bool FUSED>
+ks_status launch_hier_s(int s, const float* gy, const float* x, float* part, int64_t B,
+                        int64_t H, int64_t L, int64_t K, const HierPlan& pl, cudaStream_t st) {
+    const unsigned blocks = static_cast<unsigned>(int64_t(pl.g) * H * pl.njt);
+    const int p = static_cast<int>(K / 2);
+#define KS_HIER_CASE(SV)                                                                  \
+    case SV:                                                                              \
+        dw_hier_stage1<NJ, SV, FUSED><<<blocks, kDwThreads, 0, st>>>(                     \
+            gy, x, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L),   \
+            static_cast<int>(K), p, pl.g, pl.njt);                                        \
+        break;
+    switch (s) {
+        KS_HIER_CASE(0)
+        KS_HIER_CASE(1)
+        KS_HIER_CASE(2)
+        default:
+        KS_HIER_CASE(3)
+    }
+#undef KS_HIER_CASE
+    return check_launch();
+}
+
+template <bool FUSED>
+ks_status launch_hier(const float* gy, const float* x, float* part, int64_t B, int64_t H,
+                      int64_t L, int64_t K, const HierPlan& pl, cudaStream_t st) {
+    const int p = static_cast<int>(K / 2);
+    const int s = (4 - p % 4) % 4;
+    switch (pl.nj) {
+        case 1: return launch_hier_s<1, FUSED>(s, gy, x, part, B, H, L, K, pl, st);
+        case 2: return launch_hier_s<2, FUSED>(s, gy, x, part, B, H, L, K, pl, st);
+        case 4: return launch_hier_s<4, FUSED>(s, gy, x, part, B, H, L, K, pl, st);
+        default: return launch_hier_s<8, FUSED>(s, gy, x, part, B, H, L, K, pl, st);
+    }
+}
+
+}  // namespace
+
+size_t dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                          int elem) {
+    if (scheme == KS_DW_HIERARCHICAL) {
+        if (elem != 4) return 0;  // fp64 HIERARCHICAL runs the exact pairwise kernel
+        const HierPlan pl = hier_plan(B, H, K);
+        return size_t(pl.g) * H * K * sizeof(float);
+    }
+    if (scheme == KS_DW_PAIRWISE) return 0;
+    const int64_t nc = chunk_count(B, L, scheme, chunk);
+    const size_t bytes = size_t(nc) * H * K * elem;
+    return bytes <= kChunkWsCap ? bytes : 0;
+}
+
+template <typename T>
+static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, int64_t L,
+                          int64_t K, int scheme, int64_t chunk, int mode, void* ws,
+                          cudaStream_t st) {
+    const int64_t HK = H * K;
+    if (scheme == KS_DW_PAIRWISE || scheme == KS_DW_HIERARCHICAL) {
+        const int64_t n = B * L;
+        int D = 0;
+        while (D < 8 && (int64_t(2) << D) <= n) ++D;
+        dw_pairwise_exact<T><<<static_cast<unsigned>(HK), 256, 0, st>>>(gy, x, dk, B, H, L, K, D);
+        return check_launch();
+    }
+    const int64_t nc = chunk_count(B, L, scheme, chunk);
+    const size_t need = size_t(nc) * HK * sizeof(T);
+    if (need <= kChunkWsCap) {
+        T* part = static_cast<T*>(ws);
+        const int64_t total = nc * HK;
+        const unsigned blocks =
+            static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms()) * 64));
+        if (mode == KS_MULADD_FUSED)
+            dw_chunk_partials<T, true><<<blocks, 256, 0, st>>>(gy, x, part, B, H, L, K,
+                                                               nc == 1 ? B * L : chunk, nc);
+        else
+            dw_chunk_partials<T, false><<<blocks, 256, 0, st>>>(gy, x, part, B, H, L, K,
+                                                                nc == 1 ? B * L : chunk, nc);
+        ks_status s = check_launch();
+        if (s != KS_OK) return s;
+        dw_chunk_total<T><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, nc);
+        return check_launch();
+    }
+    const unsigned blocks = static_cast<unsigned>((HK + 127) / 128);
+    if (mode == KS_MULADD_FUSED)
+        dw_chunked_fused<T, true><<<blocks, 128, 0, st>>>(gy, x, dk, B, H, L, K, chunk, nc);
+    else
+        dw_chunked_fused<T, false><<<blocks, 128, 0, st>>>(gy, x, dk, B, H, L, K, chunk, nc);
+    return check_launch();
+}
+
+ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
+                 int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
+    if (scheme != KS_DW_HIERARCHICAL)
+        return dw_exact<float>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);
+    if (L > (1ll << 30) || K > (1ll << 30) || B > (1ll << 30))
+        return dw_exact<float>(gy, x, dk, B, H, L, K, KS_DW_PAIRWISE, 0, mode, ws, st);
+    const HierPlan pl = hier_plan(B, H, K);
+    float* part = static_cast<float*>(ws);
+    ks_status s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
+                                          : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);
+    if (s != KS_OK) return s;
+    const int64_t HK = H * K;
+    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.g);
+    return check_launch();
+}
+
+ks_status dw_f64(const double* gy, const double* x, double* dk, int64_t B, int64_t H, int64_t L,
+                 int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
+    return dw_exact<double>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);
+}
+
+}  // namespace ks

@@ -1,0 +1,146 @@
+// dist.cu -- batch sharding and the dW combine across GPUs (one process per
+// GPU).  The reference is single-process CPU code with no collectives; batch
+// sharding is the natural partition of this operator (rows (b,.,.) are
+// independent for y and dX, and dW is a sum over b), so the only exchange is
+// one reduction of the H*K weight gradient.
+//
+//  * ks_dwconv1d_dw_allreduce_f32: one ncclAllReduce(sum) over NVLink/NVSwitch.
+//  * ks_dwconv1d_dw_allgather_sum_f32: ncclAllGather of the rank partials, then
+//    a fixed pairwise tree in rank order on every rank, so the result does not
+//    depend on NCCL's algorithm/protocol choice and is bitwise identical on all
+//    ranks (and, for PAIRWISE with power-of-two shards, to the 1-GPU result).
+#include <nccl.h>
+
+#include "ks_common.cuh"
+
+struct ks_comm {
+    ncclComm_t nccl = nullptr;
+    int world = 1;
+    int rank = 0;
+};
+
+namespace ks {
+
+void set_last_error(const char* what);
+
+static ks_status nccl_status(ncclResult_t r) {
+    if (r == ncclSuccess) return KS_OK;
+    set_last_error(ncclGetErrorString(r));
+    return KS_ERR_NCCL;
+}
+
+// out[i] = pairwise tree over the `world` rank slices of gather[world][n], in
+// rank order (midpoint split, like the reference's reduce_pairwise).
+__global__ void rank_tree_sum(const float* __restrict__ gather, float* __restrict__ out,
+                              int64_t n, int world) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= n) return;
+    float v[64];
+    int w = world < 64 ? world : 64;
+    for (int r = 0; r < w; ++r) v[r] = gather[static_cast<int64_t>(r) * n + i];
+    // midpoint-split recursion, evaluated with an explicit stack
+    struct Frame { int lo, hi, state; };
+    Frame st[16];
+    float vals[16];
+    int sp = 0, vp = 0;
+    st[sp++] = {0, w, 0};
+    while (sp) {
+        Frame& f = st[sp - 1];
+        if (f.hi - f.lo == 1) {
+            vals[vp++] = v[f.lo];
+            --sp;
+            continue;
+        }
+        const int mid = f.lo + (f.hi - f.lo) / 2;
+        if (f.state == 0) {
+            f.state = 1;
+            st[sp++] = {f.lo, mid, 0};
+        } else if (f.state == 1) {
+            f.state = 2;
+            st[sp++] = {mid, f.hi, 0};
+        } else {
+            const float r = vals[--vp];
+            const float l = vals[--vp];
+            vals[vp++] = l + r;
+            --sp;
+        }
+    }
+    out[i] = vals[0];
+}
+
+}  // namespace ks
+
+using namespace ks;
+
+extern "C" {
+
+ks_status ks_shard_rows(int64_t B, int world, int rank, int64_t* b0, int64_t* nb) {
+    if (!b0 || !nb) return KS_ERR_NULL;
+    if (B < 1) return KS_ERR_DIM_B;
+    if (world < 1 || rank < 0 || rank >= world || world > B) return KS_ERR_SHARD;
+    const int64_t lo = B * rank / world;
+    const int64_t hi = B * (rank + 1) / world;
+    *b0 = lo;
+    *nb = hi - lo;
+    return KS_OK;
+}
+
+ks_status ks_comm_unique_id(void* id128) {
+    if (!id128) return KS_ERR_NULL;
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+    return nccl_status(ncclGetUniqueId(static_cast<ncclUniqueId*>(id128)));
+}
+
+ks_status ks_comm_init(ks_comm** comm, const void* id128, int world, int rank) {
+    if (!comm || !id128) return KS_ERR_NULL;
+    if (world < 1 || rank < 0 || rank >= world) return KS_ERR_SHARD;
+    ks_comm* c = new ks_comm;
+    c->world = world;
+    c->rank = rank;
+    ncclUniqueId id;
+    memcpy(&id, id128, sizeof(id));
+    const ks_status s = nccl_status(ncclCommInitRank(&c->nccl, world, id, rank));
+    if (s != KS_OK) {
+        delete c;
+        return s;
+    }
+    *comm = c;
+    return KS_OK;
+}
+
+ks_status ks_comm_destroy(ks_comm* comm) {
+    if (!comm) return KS_OK;
+    ks_status s = KS_OK;
+    if (comm->nccl) s = nccl_status(ncclCommDestroy(comm->nccl));
+    delete comm;
+    return s;
+}
+
+ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm* comm,
+                                       void* stream) {
+    if (!dk || !comm) return KS_ERR_NULL;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (K < 1) return KS_ERR_DIM_K;
+    if (comm->world == 1) return KS_OK;
+    return nccl_status(ncclAllReduce(dk, dk, static_cast<size_t>(H * K), ncclFloat, ncclSum,
+                                     comm->nccl, static_cast<cudaStream_t>(stream)));
+}
+
+ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, int64_t K,
+                                           ks_comm* comm, void* stream) {
+    if (!dk || !gather || !comm) return KS_ERR_NULL;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (K < 1) return KS_ERR_DIM_K;
+    if (comm->world > 64) return KS_ERR_SHARD;
+    if (comm->world == 1) return KS_OK;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t n = static_cast<size_t>(H * K);
+    ks_status s = nccl_status(ncclAllGather(dk, gather, n, ncclFloat, comm->nccl, st));
+    if (s != KS_OK) return s;
+    rank_tree_sum<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(gather, dk,
+                                                                          static_cast<int64_t>(n),
+                                                                          comm->world);
+    return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,59 @@
+// ks_common.cuh -- shared device helpers for the sm_100a kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "ks_dwconv1d.h"
+
+namespace ks {
+
+// Multiply-add in the reference's two rounding modes (src/conv_core.cpp:14-19).
+// The intrinsics are never contracted by nvcc, so Separate really rounds twice.
+template <bool FUSED>
+__device__ __forceinline__ float muladd(float acc, float a, float b) {
+    if constexpr (FUSED) return __fmaf_rn(a, b, acc);
+    else return __fadd_rn(acc, __fmul_rn(a, b));
+}
+template <bool FUSED>
+__device__ __forceinline__ double muladd(double acc, double a, double b) {
+    if constexpr (FUSED) return __fma_rn(a, b, acc);
+    else return __dadd_rn(acc, __dmul_rn(a, b));
+}
+
+// Shared-memory window layout: 4 floats of padding after every 32, so float4
+// reads by lanes 32 B or 64 B apart (the register-tile strides used below)
+// hit 8 distinct 16-byte bank groups per quarter-warp phase.  A float4 at a
+// 4-aligned logical index never straddles a pad.
+__device__ __forceinline__ int pad_idx(int i) { return i + ((i >> 5) << 2); }
+__host__ __device__ constexpr int padded_len(int n) { return n + ((n + 31) >> 5) * 4 + 4; }
+
+__device__ __forceinline__ float4 ld_nc_v4(const float* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_cs_v4(float* p, float4 v) {
+    asm volatile("st.global.cs.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w)
+                 : "memory");
+}
+
+inline int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+// Records a CUDA error for ks_last_error_string and maps it to a status.
+ks_status cuda_status(cudaError_t e);
+ks_status check_launch();
+
+}  // namespace ks
