@@ -465,6 +465,10 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
     return check_launch();
 }
 
+ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int, int,
+                        int, cudaStream_t, bool*);
+bool tma_disabled();
+
 ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                  int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
     if (scheme != KS_DW_HIERARCHICAL)
@@ -473,8 +477,12 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
         return dw_exact<float>(gy, x, dk, B, H, L, K, KS_DW_PAIRWISE, 0, mode, ws, st);
     const HierPlan pl = hier_plan(B, H, K);
     float* part = static_cast<float*>(ws);
-    ks_status s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
-                                          : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);
+    bool handled = false;
+    ks_status s = KS_OK;
+    if (!tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.nj, pl.njt, pl.g, mode, st, &handled);
+    if (!handled)
+        s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
+                                    : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
     dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.g);

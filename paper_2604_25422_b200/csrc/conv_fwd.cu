@@ -19,6 +19,7 @@
 // window over the taps in blocks of JB, so every shared-memory word feeds
 // R*JB/(R+JB) FMAs.  Stores are 128-bit streaming stores.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 
@@ -214,10 +215,26 @@ static ks_status launch_direct(const T* in, const T* k, T* out, int64_t B, int64
     return check_launch();
 }
 
+ks_status stencil_tma_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
+                          int, int, cudaStream_t, bool*);
+
+bool tma_disabled() {
+    static const bool off = [] {
+        const char* e = getenv("KS_DISABLE_TMA");
+        return e && e[0] == '1';
+    }();
+    return off;
+}
+
 // Entry used by the C ABI for both fp32 paths (shapes already validated).
 ks_status conv_stencil_f32(const float* in, const float* k, float* out, int64_t B, int64_t H,
                            int64_t L, int64_t K, int64_t off, int reverse, int mode,
                            cudaStream_t st) {
+    if (!tma_disabled()) {
+        bool handled = false;
+        const ks_status s = stencil_tma_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
+        if (handled) return s;
+    }
     // Register tile of 16 outputs for long rows, 4 for short ones so small-L
     // problems still spread over many CTAs.
     const bool small = L <= 1024;
