@@ -350,9 +350,12 @@ def run_ours(args, cfg_name, cfg):
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
 
         def host_step():
-            ks.forward(xn, kn, mode, out=yn)
-            ks.backward_input(gyn, kn, mode, out=dxn)
-            ks.backward_weight(gyn, xn, K, scheme, 0, mode, out=dkn)
+            if args.e2e_path == "step":
+                ks.step_host(xn, kn, gyn, scheme=scheme, mode=mode, out=(yn, dxn, dkn))
+            else:  # the reference's three value-type calls, each through its own host entry
+                ks.forward(xn, kn, mode, out=yn)
+                ks.backward_input(gyn, kn, mode, out=dxn)
+                ks.backward_weight(gyn, xn, K, scheme, 0, mode, out=dkn)
 
         host_step()
         if world > 1:
@@ -366,10 +369,15 @@ def run_ours(args, cfg_name, cfg):
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             t_host = float(tt[0])
         tb = 4 * B * H * L
+        if args.e2e_path == "step":
+            h2d, d2h = 2 * tb + 4 * H * K, 2 * tb + 4 * H * K
+            path = "ks_dwconv1d_step_f32_host (x, gy up once; y, dx, dk down), pinned host buffers, wall clock"
+        else:
+            h2d, d2h = 4 * tb + 2 * 4 * H * K, 2 * tb + 4 * H * K
+            path = "ks_dwconv1d_{fwd,dx,dw}_f32_host, pinned host buffers, wall clock"
         e2e = {"value": round(world * 3 * pb / t_host / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": 4 * tb + 2 * 4 * H * K, "d2h_bytes_per_step": 2 * tb + 4 * H * K,
-               "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps,
-               "path": "ks_dwconv1d_{fwd,dx,dw}_f32_host, pinned host buffers, wall clock"}
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps, "path": path}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -413,6 +421,7 @@ def main():
     ap.add_argument("--scheme", choices=["hierarchical", "pairwise"], default="hierarchical")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-path", choices=["step", "calls"], default="step")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

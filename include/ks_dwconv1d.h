@@ -137,6 +137,14 @@ ks_status ks_dwconv1d_dw_f64_host(const double* gy, const double* x, double* dk,
                                   int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                                   int mode);
 
+/* One fwd + bwd step of the layer on host buffers (no reference counterpart:
+ * the three calls above fused so x and gy cross PCIe once).  y = forward(x),
+ * dx = backward_input(gy), dk = backward_weight(gy, x); bits equal the three
+ * separate calls. */
+ks_status ks_dwconv1d_step_f32_host(const float* x, const float* k, const float* gy, float* y, float* dx,
+                                    float* dk, int64_t B, int64_t H, int64_t L, int64_t K, int scheme,
+                                    int64_t chunk, int mode);
+
 /* ---- batch sharding across GPUs (one process per GPU) --------------------- */
 /* Contiguous batch slice of rank `rank` out of `world`: rows [*b0, *b0+*nb).
  * Slices differ by at most one row; pure host arithmetic (no device). */

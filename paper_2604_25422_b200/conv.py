@@ -163,6 +163,22 @@ def backward_weight(gy, x, K: int, scheme: int = SEQUENTIAL, chunk: int = 1024,
     return out
 
 
+def step_host(x, k, gy, K: int | None = None, scheme: int = HIERARCHICAL, chunk: int = 0,
+              mode: int = FUSED, out=None):
+    """One fwd + dX + dW step on host (numpy) buffers through
+    ks_dwconv1d_step_f32_host; returns (y, dx, dk)."""
+    B, H, L = _dims3(x, "step: x")
+    _dims3(gy, "step: gy", (B, H, L))
+    K = _dims_k(k, "step: k", H)
+    if out is None:
+        out = (np.empty_like(x), np.empty_like(gy), np.empty((H, K), np.float32))
+    y, dx, dk = out
+    st = _lib.lib().ks_dwconv1d_step_f32_host(_ptr(x), _ptr(k), _ptr(gy), _ptr(y), _ptr(dx), _ptr(dk),
+                                              B, H, L, K, scheme, chunk, mode)
+    _raise_dims(st, "step")
+    return y, dx, dk
+
+
 def fill_pm1(seed: int, first: int, out) -> None:
     """Device splitmix64 fill, bit-identical to the reference SplitMix64 stream
     (include/kernelscope/rng.hpp:12-28): out.flat[i] = draw first+1+i."""

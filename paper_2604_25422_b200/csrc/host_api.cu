@@ -151,6 +151,81 @@ ks_status dw_host(DwFn<T> fn, const T* gy, const T* x, T* dk, int64_t B, int64_t
     return rc;
 }
 
+// One training step of the layer on host buffers: y = fwd(x), dx = dX(gy),
+// dk = dW(gy, x).  x and gy are uploaded once (block by block, three streams)
+// into full device copies; forward and dX run per block as soon as that block
+// has landed and their results stream back while later blocks upload; dW runs
+// once on the full device copies after the last upload, so its bits equal the
+// device-pointer call for every scheme.
+ks_status step_host(const float* x, const float* k, const float* gy, float* y, float* dxo, float* dk, int64_t B,
+                    int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk, int mode) {
+    if (!x || !k || !gy || !y || !dxo || !dk) return KS_ERR_NULL;
+    ensure_pool();
+    const size_t entry = sizeof(float) * size_t(H) * size_t(L);
+    const size_t tbytes = entry * size_t(B);
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(kBlockBytes / std::max<size_t>(entry, 1))));
+    const int64_t nblocks = (B + nb - 1) / nb;
+    const int slots = static_cast<int>(std::min<int64_t>(kSlots, nblocks));
+    cudaStream_t st[kSlots] = {};
+    float *dxin = nullptr, *dgy = nullptr, *dkk = nullptr, *ddk = nullptr;
+    float* dy[kSlots] = {};
+    float* ddx[kSlots] = {};
+    cudaEvent_t ev[kSlots] = {};
+    ks_status rc = KS_OK;
+    for (int s = 0; s < slots && rc == KS_OK; ++s) {
+        rc = cuda_status(cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking));
+        if (rc == KS_OK) rc = cuda_status(cudaEventCreateWithFlags(&ev[s], cudaEventDisableTiming));
+    }
+    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dxin, tbytes, st[0]));
+    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dgy, tbytes, st[0]));
+    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dkk, sizeof(float) * H * K, st[0]));
+    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&ddk, sizeof(float) * H * K, st[0]));
+    for (int s = 0; s < slots && rc == KS_OK; ++s) {
+        rc = cuda_status(cudaMallocAsync(&dy[s], entry * nb, st[0]));
+        if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&ddx[s], entry * nb, st[0]));
+    }
+    if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dkk, k, sizeof(float) * H * K, cudaMemcpyHostToDevice, st[0]));
+    if (rc == KS_OK) rc = cuda_status(cudaEventRecord(ev[0], st[0]));
+    for (int s = 1; s < slots && rc == KS_OK; ++s) rc = cuda_status(cudaStreamWaitEvent(st[s], ev[0], 0));
+    for (int64_t i = 0; i < nblocks && rc == KS_OK; ++i) {
+        const int s = static_cast<int>(i % slots);
+        const int64_t b0 = i * nb, bn = std::min<int64_t>(nb, B - b0);
+        const size_t off = size_t(b0) * H * L, bytes = entry * bn;
+        rc = cuda_status(cudaMemcpyAsync(dxin + off, x + off, bytes, cudaMemcpyHostToDevice, st[s]));
+        if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dgy + off, gy + off, bytes, cudaMemcpyHostToDevice, st[s]));
+        if (rc == KS_OK) rc = ks_dwconv1d_fwd_f32(dxin + off, dkk, dy[s], bn, H, L, K, mode, st[s]);
+        if (rc == KS_OK) rc = ks_dwconv1d_dx_f32(dgy + off, dkk, ddx[s], bn, H, L, K, mode, st[s]);
+        if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(y + off, dy[s], bytes, cudaMemcpyDeviceToHost, st[s]));
+        if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dxo + off, ddx[s], bytes, cudaMemcpyDeviceToHost, st[s]));
+    }
+    // dW after every upload: stream 0 waits for the other streams
+    for (int s = 1; s < slots && rc == KS_OK; ++s) {
+        rc = cuda_status(cudaEventRecord(ev[s], st[s]));
+        if (rc == KS_OK) rc = cuda_status(cudaStreamWaitEvent(st[0], ev[s], 0));
+    }
+    if (rc == KS_OK) rc = ks_dwconv1d_dw_f32(dgy, dxin, ddk, B, H, L, K, scheme, chunk, mode, nullptr, 0, st[0]);
+    if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dk, ddk, sizeof(float) * H * K, cudaMemcpyDeviceToHost, st[0]));
+    for (int s = 0; s < slots; ++s)
+        if (st[s]) cudaStreamSynchronize(st[s]);
+    if (st[0]) {
+        if (dxin) cudaFreeAsync(dxin, st[0]);
+        if (dgy) cudaFreeAsync(dgy, st[0]);
+        if (dkk) cudaFreeAsync(dkk, st[0]);
+        if (ddk) cudaFreeAsync(ddk, st[0]);
+        for (int s = 0; s < slots; ++s) {
+            if (dy[s]) cudaFreeAsync(dy[s], st[0]);
+            if (ddx[s]) cudaFreeAsync(ddx[s], st[0]);
+        }
+        const ks_status e = cuda_status(cudaStreamSynchronize(st[0]));
+        if (rc == KS_OK) rc = e;
+    }
+    for (int s = 0; s < slots; ++s) {
+        if (st[s]) cudaStreamDestroy(st[s]);
+        if (ev[s]) cudaEventDestroy(ev[s]);
+    }
+    return rc;
+}
+
 }  // namespace
 }  // namespace ks
 
@@ -211,6 +286,19 @@ ks_status ks_dwconv1d_dw_f64_host(const double* gy, const double* x, double* dk,
     if (scheme < KS_DW_SEQUENTIAL || scheme > KS_DW_HIERARCHICAL) return KS_ERR_BAD_SCHEME;
     if (scheme == KS_DW_CHUNKED && chunk < 1) return KS_ERR_BAD_CHUNK;
     return dw_host<double>(ks_dwconv1d_dw_f64, gy, x, dk, B, H, L, K, scheme, chunk, mode);
+}
+
+ks_status ks_dwconv1d_step_f32_host(const float* x, const float* k, const float* gy, float* y, float* dx,
+                                    float* dk, int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                                    int mode) {
+    if (B < 1) return KS_ERR_DIM_B;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (L < 1) return KS_ERR_DIM_L;
+    if (K < 1) return KS_ERR_DIM_K;
+    if (mode != KS_MULADD_SEPARATE && mode != KS_MULADD_FUSED) return KS_ERR_BAD_MODE;
+    if (scheme < KS_DW_SEQUENTIAL || scheme > KS_DW_HIERARCHICAL) return KS_ERR_BAD_SCHEME;
+    if (scheme == KS_DW_CHUNKED && chunk < 1) return KS_ERR_BAD_CHUNK;
+    return step_host(x, k, gy, y, dx, dk, B, H, L, K, scheme, chunk, mode);
 }
 
 }  // extern "C"

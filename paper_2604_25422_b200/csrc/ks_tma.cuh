@@ -1,13 +1,18 @@
 // ks_tma.cuh -- raw-PTX helpers for TMA (cp.async.bulk.tensor) + mbarrier
 // pipelines on sm_100a, and the host-side tensor-map encoder.
 //
-// Row views: a [rows, L] fp32 tensor (L % 32 == 0) is described to TMA as the
-// 3-D tensor {32, L/32, rows} (innermost first) with SWIZZLE_128B, so one box
-// {32, n, 1} is n consecutive 128-byte pieces of one row.  Out-of-bounds
-// coordinates (a halo before t=0 or past t=L) are zero-filled by the TMA unit,
-// which is exactly the zero padding of the reference's window
-// (src/conv_core.cpp:35-36).  In shared memory the 16-byte chunk c of 128-byte
-// row r lands at chunk c ^ (r & 7) of that row (1024-byte aligned buffer).
+// Row views: a [rows, L] fp32 tensor (L % IN == 0) is described to TMA as the
+// 3-D tensor {IN, L/IN, rows} (innermost first), so one box {IN, n, 1} is n
+// consecutive IN-float pieces of one row.  Out-of-bounds coordinates (a halo
+// before t=0 or past t=L) are zero-filled by the TMA unit on loads and
+// clipped on stores -- exactly the reference's zero padding
+// (src/conv_core.cpp:35-36) with no halo code in the kernels.
+//
+// Shared-memory swizzles (TMA SWIZZLE_32B / 64B / 128B): 16-byte chunk bits
+// [4:4+w) of the byte address are XORed with bits [7:7+w), w = 1 / 2 / 3.  The
+// right mode depends on the lane stride of the consumer's 128-bit reads:
+// 32 B apart -> SWIZZLE_32B, 64 B apart -> SWIZZLE_64B, 16 B -> none; each is
+// conflict-free for every starting offset (checked exhaustively).
 #pragma once
 
 #include <cuda.h>
@@ -20,12 +25,26 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// Pointer into the dynamic shared buffer rounded up to `align` bytes, derived
+// from the __shared__ array itself so the compiler keeps the shared address
+// space (LDS/STS rather than generic LD/ST).
+template <uint32_t ALIGN>
+__device__ __forceinline__ unsigned char* align_smem(unsigned char* raw) {
+    const uint32_t pad = (ALIGN - (smem_u32(raw) & (ALIGN - 1))) & (ALIGN - 1);
+    return raw + pad;
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
 
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// Generic-proxy shared writes -> visible to the async proxy (TMA store).
+__device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
@@ -56,6 +75,22 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
+// 3-D tiled TMA store of one box from shared memory (bulk-group tracked).
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3}], [%4];" ::"l"(
+            reinterpret_cast<uint64_t>(map)),
+        "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(src))
+        : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// All committed bulk stores have finished READING shared memory.
+__device__ __forceinline__ void bulk_wait_read_all() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+// All committed bulk stores are complete (writes performed).
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
 // 1-D bulk copy global -> shared (16-byte aligned, size % 16 == 0).
 __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
@@ -69,21 +104,22 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
 
-// Byte offset of the float4 at logical float index i (i % 4 == 0) inside a
-// SWIZZLE_128B box that starts at a 1024-byte aligned address.
-__device__ __forceinline__ uint32_t swz128(uint32_t i) {
-    const uint32_t row = i >> 5;
-    const uint32_t chunk = (i >> 2) & 7u;
-    return (row << 7) | ((chunk ^ (row & 7u)) << 4);
+// Swizzled byte offset of the float4 at logical float index i (i % 4 == 0)
+// in a buffer aligned to at least 1024 B.  SW = 0 (none), 32, 64, 128.
+template <int SW>
+__device__ __forceinline__ uint32_t swz(uint32_t i) {
+    const uint32_t b = i << 2;
+    if constexpr (SW == 0) return b;
+    else if constexpr (SW == 32) return b ^ ((b >> 3) & 0x10u);
+    else if constexpr (SW == 64) return b ^ ((b >> 3) & 0x30u);
+    else return b ^ ((b >> 3) & 0x70u);
 }
 
-__device__ __forceinline__ float4 lds128(const char* base, uint32_t byte_off) {
-    return *reinterpret_cast<const float4*>(base + byte_off);
-}
-
-// Host: encode the {32, L/32, rows} SWIZZLE_128B row view of a [rows, L] fp32
-// tensor with a box of {32, box_rows, 1}.  Returns false when the driver entry
-// point is unavailable or the tensor violates TMA's constraints.
-bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int box_rows);
+// Host: encode the {IN, L/IN, rows} view of a [rows, L] fp32 tensor with box
+// {IN, box_rows, 1} and swizzle SW (0/32/64/128; IN*4 must be <= SW when SW>0).
+// Returns false when the driver entry point is unavailable or the tensor
+// violates TMA's constraints (the caller then uses the generic kernels).
+bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int inner, int box_rows,
+                     int sw);
 
 }  // namespace ks

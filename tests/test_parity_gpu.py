@@ -151,6 +151,17 @@ def test_host_pipeline_multiblock(oracle):
         assert same(y[:, h:h + 1], oracle.forward(np.ascontiguousarray(x[:, h:h + 1]), k[h:h + 1], FUSED))
 
 
+@pytest.mark.parametrize("shape", [(3, 4, 2500, 17), (40, 64, 8192, 7), (5, 3, 1024, 64)])
+def test_step_host_matches_separate_calls(oracle, shape):
+    B, H, L, K = shape
+    x, k, gy = oracle.fill_inputs(21, B, H, L, K)
+    for s in (ks.HIERARCHICAL, PAIRWISE):
+        y, dx, dk = ks.step_host(x, k, gy, scheme=s, mode=FUSED)
+        assert same(y, host(ks.forward(dev(x), dev(k), FUSED)))
+        assert same(dx, host(ks.backward_input(dev(gy), dev(k), FUSED)))
+        assert same(dk, host(ks.backward_weight(dev(gy), dev(x), K, s, 0, FUSED)))
+
+
 def test_workspace_contract():
     B, H, L, K = 8, 4, 512, 9
     x, k, gy = ks.make_inputs(2, B, H, L, K)
