@@ -306,6 +306,17 @@ def run_ours(args, cfg_name, cfg):
         ms_total, per_mean = float(t[0]), t[1:].cpu().numpy()
     ms_step = ms_total / args.steps
 
+    if args.timing_log and rank == 0:
+        # the reference's timing-log schema (src/timing_log.cpp:44-97): one row
+        # per path per timed step; conv_total = fwd + bwd_in + bwd_k
+        with open(args.timing_log, "w") as f:
+            f.write("# kernelscope timing log from the B200 library (bench.py); variant b200_tma\n")
+            f.write("variant,path,runtime_ms,run_id\n")
+            for i, row in enumerate(per):
+                for name, v in zip(("fwd", "bwd_in", "bwd_k"), row[:3]):
+                    f.write(f"b200_tma,{name},{v:.6f},{i}\n")
+                f.write(f"b200_tma,conv_total,{float(sum(row[:3])):.6f},{i}\n")
+
     pb = path_bytes(B, H, L, K)
     value = world * 3 * pb / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
@@ -422,6 +433,8 @@ def main():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-path", choices=["step", "calls"], default="step")
+    ap.add_argument("--timing-log", default=None,
+                    help="also write per-step path times in the reference's timing CSV schema")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -414,6 +414,11 @@ ks_status launch_hier(const float* gy, const float* x, float* part, int64_t B, i
 
 }  // namespace
 
+size_t dw_pairwise_tma_workspace(int64_t B, int64_t H, int64_t L, int64_t K);
+ks_status dw_pairwise_tma_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
+                              int64_t K, void* ws, cudaStream_t st, bool* handled);
+bool tma_disabled();
+
 size_t dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                           int elem) {
     if (scheme == KS_DW_HIERARCHICAL) {
@@ -421,7 +426,7 @@ size_t dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme
         const HierPlan pl = hier_plan(B, H, K);
         return size_t(pl.g) * H * K * sizeof(float);
     }
-    if (scheme == KS_DW_PAIRWISE) return 0;
+    if (scheme == KS_DW_PAIRWISE) return elem == 4 ? dw_pairwise_tma_workspace(B, H, L, K) : 0;
     const int64_t nc = chunk_count(B, L, scheme, chunk);
     const size_t bytes = size_t(nc) * H * K * elem;
     return bytes <= kChunkWsCap ? bytes : 0;
@@ -465,12 +470,16 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
     return check_launch();
 }
 
-ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int, int,
-                        int, cudaStream_t, bool*);
-bool tma_disabled();
+ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
+                        cudaStream_t, bool*);
 
 ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                  int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
+    if (scheme == KS_DW_PAIRWISE && !tma_disabled()) {
+        bool handled = false;
+        const ks_status s = dw_pairwise_tma_f32(gy, x, dk, B, H, L, K, ws, st, &handled);
+        if (handled) return s;
+    }
     if (scheme != KS_DW_HIERARCHICAL)
         return dw_exact<float>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);
     if (L > (1ll << 30) || K > (1ll << 30) || B > (1ll << 30))
@@ -479,7 +488,7 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
     float* part = static_cast<float*>(ws);
     bool handled = false;
     ks_status s = KS_OK;
-    if (!tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.nj, pl.njt, pl.g, mode, st, &handled);
+    if (!tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
     if (!handled)
         s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
                                     : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);

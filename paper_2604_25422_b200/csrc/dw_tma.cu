@@ -1,0 +1,248 @@
+// dw_tma.cu -- TMA-pipelined weight gradient, HIERARCHICAL order (sm_100a),
+// rows with L % 32 == 0.
+//
+//   dk[h,j] = sum_b sum_t gy[b,h,t] * x[b,h,t+j-p]     (reference src/conv_core.cpp:148-181)
+//
+// CTA = (row group g, channel h, tap tile of JT = NJ*JR taps); 256 threads =
+// NJ tap groups x NTS t-slices.  Work items are (row b, 2048-wide t tile) in
+// flat order; each of NS stages holds the gy tile and the x window
+// [t0+j0-p-D, ...) (TMA, zero outside the row), completing on an mbarrier.
+// Thread (tap group, t-slice) reads TB gy values and TB+JR-1 x values per
+// register block with 128-bit conflict-free loads (lanes 128 B apart under
+// SWIZZLE_128B) and accumulates JR taps x TB t FMAs into JR registers -- the
+// in-register partial sums over L.  Then a fixed xor-shuffle tree per warp, a
+// fixed pass over the warps of each tap group, one partial per CTA into
+// part[g,h,j]; dw_sum_groups (conv_dw.cu) adds the G partials in ascending g.
+// No atomics anywhere: the result is a deterministic function of the shape.
+//
+// (JR, TB) = (8, 8) for K <= 8 (memory-bound, e.g. BASELINE config 3) and
+// (16, 16) for longer K, where 256 FMAs per 13 shared loads keep the FMA pipe
+// fed (compute-bound, configs 2 / 4 / 5b / 5c).
+#include <algorithm>
+
+#include "ks_common.cuh"
+#include "ks_tma.cuh"
+
+namespace ks {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kDwTT = 2048;              // t per work item
+constexpr int kDwIn = 32;                // floats per TMA row piece (128 B)
+constexpr int kDwMain = kDwTT / kDwIn;   // x window main-box rows
+
+struct DwGeomT {
+    int XR;           // x window rows (32 floats): kDwMain main + XT tail
+    int XT;           // tail rows
+    int gy_bytes;     // kDwTT*4
+    int stage_bytes;
+};
+
+// Register block `q` (0 <= q < TT/TB) -> first t of the block; consecutive
+// lanes get blocks 128 B apart.
+template <int TB>
+__device__ __forceinline__ int block_t(int q) {
+    if constexpr (TB == 8) return ((q & 31) * 4 + ((q >> 5) & 3) + (q >> 7) * 128) * TB;
+    else return ((q & 31) * 2 + ((q >> 5) & 1) + (q >> 6) * 64) * TB;
+}
+
+template <int JR, int TB, int NJ, int S, bool FUSED>
+__global__ void __launch_bounds__(kThreads)
+dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUtensorMap x_map,
+       const __grid_constant__ CUtensorMap x_tail_map, float* __restrict__ part, int B, int H, int L, int K, int p,
+       int G, int NJT, DwGeomT g, int NS) {
+    constexpr int NTS = kThreads / NJ;
+    constexpr int JT = NJ * JR;
+    constexpr int SPT = kDwTT / (NTS * TB);
+    constexpr int NVX = (S + TB + JR - 1 + 3) / 4;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = align_smem<1024>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * g.stage_bytes);
+    __shared__ float red[kThreads / 32][JR];
+
+    int bid = blockIdx.x;
+    const int jt = bid % NJT;
+    bid /= NJT;
+    const int h = bid % H;
+    const int grp = bid / H;
+    const int b_begin = static_cast<int>(static_cast<int64_t>(B) * grp / G);
+    const int b_end = static_cast<int>(static_cast<int64_t>(B) * (grp + 1) / G);
+    const int j0 = jt * JT;
+    const int tid = threadIdx.x;
+    const int jg = tid / NTS;
+    const int ts = tid - jg * NTS;
+    const int ntt = (L + kDwTT - 1) / kDwTT;
+    const int nunits = (b_end - b_begin) * ntt;
+    // the x window of a work item at t0 starts at position t0 + j0 - p - D
+    const int xoff = j0 - p;
+    const int D = ((xoff % kDwIn) + kDwIn) % kDwIn;
+    const int xr_rel = (xoff - D) / kDwIn;  // exact division
+    const int A = D & ~3;                   // D & 3 == S
+
+    if (tid == 0) {
+        prefetch_tmap(&gy_map);
+        prefetch_tmap(&x_map);
+        prefetch_tmap(&x_tail_map);
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    const uint32_t tx_bytes = static_cast<uint32_t>(g.gy_bytes + g.XR * kDwIn * 4);
+    auto issue = [&](int stage, int u) {
+        const int b = b_begin + u / ntt;
+        const int t0 = (u % ntt) * kDwTT;
+        const int row = b * H + h;
+        unsigned char* sb = smem + stage * g.stage_bytes;
+        mbar_arrive_expect_tx(&full[stage], tx_bytes);
+        tma_load_3d(sb, &gy_map, 0, t0 / kDwIn, row, &full[stage]);
+        const int xr = t0 / kDwIn + xr_rel;
+        tma_load_3d(sb + g.gy_bytes, &x_map, 0, xr, row, &full[stage]);
+        tma_load_3d(sb + g.gy_bytes + kDwMain * kDwIn * 4, &x_tail_map, 0, xr + kDwMain, row, &full[stage]);
+    };
+    if (tid == 0)
+        for (int s = 0; s < NS && s < nunits; ++s) issue(s, s);
+
+    float acc[JR];
+#pragma unroll
+    for (int i = 0; i < JR; ++i) acc[i] = 0.f;
+
+    for (int u = 0; u < nunits; ++u) {
+        const int stage = u % NS;
+        mbar_wait(&full[stage], static_cast<uint32_t>((u / NS) & 1));
+        const unsigned char* gys = smem + stage * g.stage_bytes;
+        const unsigned char* xs = gys + g.gy_bytes;
+        const int t0 = (u % ntt) * kDwTT;
+#pragma unroll 2
+        for (int s = 0; s < SPT; ++s) {
+            const int tl = block_t<TB>(s * NTS + ts);
+            if (t0 + tl < L) {
+                float gv[TB];
+#pragma unroll
+                for (int c = 0; c < TB / 4; ++c) {
+                    const float4 q = *reinterpret_cast<const float4*>(gys + swz<128>(static_cast<uint32_t>(tl + 4 * c)));
+                    gv[4 * c + 0] = q.x;
+                    gv[4 * c + 1] = q.y;
+                    gv[4 * c + 2] = q.z;
+                    gv[4 * c + 3] = q.w;
+                }
+                float xv[4 * NVX];
+                const uint32_t xi = static_cast<uint32_t>(A + tl + jg * JR);
+#pragma unroll
+                for (int c = 0; c < NVX; ++c) {
+                    const float4 q = *reinterpret_cast<const float4*>(xs + swz<128>(xi + 4 * c));
+                    xv[4 * c + 0] = q.x;
+                    xv[4 * c + 1] = q.y;
+                    xv[4 * c + 2] = q.z;
+                    xv[4 * c + 3] = q.w;
+                }
+#pragma unroll
+                for (int tt = 0; tt < TB; ++tt)
+#pragma unroll
+                    for (int jj = 0; jj < JR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+            }
+        }
+        __syncthreads();
+        if (tid == 0 && u + NS < nunits) issue(stage, u + NS);
+    }
+
+#pragma unroll
+    for (int jj = 0; jj < JR; ++jj) {
+        float v = acc[jj];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        acc[jj] = v;
+    }
+    const int warp = tid >> 5, lane = tid & 31;
+    if (lane == 0) {
+#pragma unroll
+        for (int jj = 0; jj < JR; ++jj) red[warp][jj] = acc[jj];
+    }
+    __syncthreads();
+    constexpr int WPG = NTS / 32;  // warps per tap group
+    if (tid < JT) {
+        const int gj = tid / JR, jj = tid % JR;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < WPG; ++w) s += red[gj * WPG + w][jj];
+        const int j = j0 + tid;
+        if (j < K) part[(static_cast<int64_t>(grp) * H + h) * K + j] = s;
+    }
+}
+
+template <int JR, int TB, int NJ, bool FUSED>
+ks_status launch(int s, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt, float* part, int64_t B,
+                 int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
+    const int smem = NS * g.stage_bytes + 64 + 1024;
+    const unsigned blocks = static_cast<unsigned>(int64_t(G) * H * NJT);
+    const int p = static_cast<int>(K / 2);
+#define KS_DW_CASE(SV)                                                                                        \
+    case SV: {                                                                                                \
+        auto kern = dw_tma<JR, TB, NJ, SV, FUSED>;                                                            \
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                        \
+        kern<<<blocks, kThreads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),      \
+                                             static_cast<int>(L), static_cast<int>(K), p, G, NJT, g, NS);     \
+        break;                                                                                                \
+    }
+    switch (s) {
+        KS_DW_CASE(0)
+        KS_DW_CASE(1)
+        KS_DW_CASE(2)
+        default:
+        KS_DW_CASE(3)
+    }
+#undef KS_DW_CASE
+    return check_launch();
+}
+
+template <int JR, int TB, int NJ>
+ks_status launch_m(int s, bool fused, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt,
+                   float* part, int64_t B, int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS,
+                   cudaStream_t st) {
+    return fused ? launch<JR, TB, NJ, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
+                 : launch<JR, TB, NJ, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
+}
+
+}  // namespace
+
+// Stage 1 of HIERARCHICAL dW through TMA into part[G,H,K] (G = the caller's row
+// groups; stage 2 is shared with the generic path).  *handled = false means
+// the shape is not supported here and the caller falls back.
+ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+                        int G, int mode, cudaStream_t st, bool* handled) {
+    *handled = false;
+    if (L % kDwIn != 0 || B * H >= (int64_t(1) << 31) || L >= (int64_t(1) << 30) || K >= (int64_t(1) << 30))
+        return KS_OK;
+    // (8,8) with 1-2 tap groups up to K = 16; (16,16) with >= 2 tap groups beyond
+    // (a t-slice must cover a whole 16-wide block of the 2048-wide work item)
+    const int JR = K <= 16 ? 8 : 16;
+    int nj = JR == 8 ? 1 : 2;
+    while (nj < 8 && nj * JR < K) nj *= 2;
+    const int njt = static_cast<int>((K + nj * JR - 1) / (nj * JR));
+    if (int64_t(G) * H * njt >= (int64_t(1) << 31)) return KS_OK;
+    DwGeomT g;
+    g.gy_bytes = kDwTT * 4;
+    g.XT = (nj * JR + 40 + kDwIn - 1) / kDwIn;  // covers D + JT + the register-window overrun
+    g.XR = kDwMain + g.XT;
+    g.stage_bytes = (g.gy_bytes + g.XR * kDwIn * 4 + 1023) / 1024 * 1024;
+    CUtensorMap gm, xm, xt;
+    if (!encode_row_view(&gm, gy, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+    if (!encode_row_view(&xm, x, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+    if (!encode_row_view(&xt, x, B * H, L, kDwIn, g.XT, 128)) return KS_OK;
+    const int NS = std::max(2, std::min(4, (72 * 1024) / g.stage_bytes));
+    const int p = static_cast<int>(K / 2);
+    const int s = (4 - p % 4) % 4;
+    const bool fused = mode == KS_MULADD_FUSED;
+    *handled = true;
+    if (JR == 8)
+        return nj == 1 ? launch_m<8, 8, 1>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st)
+                       : launch_m<8, 8, 2>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+    switch (nj) {
+        case 2: return launch_m<16, 16, 2>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+        case 4: return launch_m<16, 16, 4>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+        default: return launch_m<16, 16, 8>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+    }
+}
+
+}  // namespace ks

@@ -46,7 +46,10 @@ def host(t):
 
 SHAPES = [(1, 1, 3, 3), (2, 3, 17, 5), (2, 2, 5, 4), (3, 2, 33, 8), (2, 2, 10, 16), (4, 3, 64, 1),
           (2, 2, 7, 12), (1, 2, 300, 7), (2, 1, 1030, 64), (3, 2, 4099, 9), (2, 2, 257, 200),
-          (1, 1, 5000, 33), (2, 1, 8192, 7), (1, 2, 1001, 2), (2, 2, 6, 40), (1, 1, 4096, 4096)]
+          (1, 1, 5000, 33), (2, 1, 8192, 7), (1, 2, 1001, 2), (2, 2, 6, 40), (1, 1, 4096, 4096),
+          # one shape per TMA kernel variant (register tile R x threads NT, dW tap blocking)
+          (2, 2, 2048, 33), (1, 2, 4096, 100), (1, 1, 8192, 48), (2, 2, 1024, 48), (2, 1, 2048, 12),
+          (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256)]
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -67,6 +70,21 @@ def test_dw_reference_schemes_bitwise(oracle, shape):
                      (CHUNKED, 10 ** 12)):
             got = host(ks.backward_weight(dev(gy), dev(x), K, s, c, m))
             assert same(got, oracle.backward_weight(gy, x, K, s, c, m)), (s, c, m)
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 2048, 7), (4, 2, 4096, 20), (1, 1, 8192, 64), (2, 1, 2048, 100),
+                                   (8, 2, 2048, 16), (2, 2, 4096, 3), (1, 1, 2048, 1), (2, 1, 2048, 2047)])
+def test_dw_pairwise_fast_path_bitwise(oracle, shape):
+    """The TMA pairwise kernel (power-of-two B and L >= 2048) reproduces the
+    reference's midpoint tree bit for bit, including masked edge leaves."""
+    B, H, L, K = shape
+    x, k, gy = oracle.fill_inputs(7 + K, B, H, L, K)
+    got = host(ks.backward_weight(dev(gy), dev(x), K, PAIRWISE))
+    assert same(got, oracle.backward_weight(gy, x, K, PAIRWISE))
+    # sign-of-zero corner: an all-zero gy must give +0 everywhere, like the reference
+    z = np.zeros_like(gy)
+    got0 = host(ks.backward_weight(dev(z), dev(x), K, PAIRWISE))
+    assert same(got0, oracle.backward_weight(z, x, K, PAIRWISE))
 
 
 @pytest.mark.parametrize("shape", SHAPES)
@@ -206,6 +224,11 @@ def test_full_config_channel_slices(oracle, cfg):
         if h == 0 or B * L * K <= 2 ** 26:
             truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
             assert normwise(dk[h:h + 1].cpu().numpy(), truth) <= HIER_TOL
+    if B * L * K <= 2 ** 26:  # config 3: the PAIRWISE fast path, bitwise per channel
+        dkp = host(ks.backward_weight(gy, x, K, PAIRWISE))
+        for h in (0, H - 1):
+            xs, gs = _channel_slice(x, h), _channel_slice(gy, h)
+            assert same(dkp[h:h + 1], oracle.backward_weight(gs, xs, K, PAIRWISE))
     del x, gy, y, dx
     torch.cuda.empty_cache()
 

@@ -1,0 +1,39 @@
+"""Small cases for compute-sanitizer (memcheck / racecheck / synccheck).
+
+usage (GPU box):
+  compute-sanitizer --tool memcheck  python tools/sanitize_cases.py
+  compute-sanitizer --tool racecheck python tools/sanitize_cases.py
+Covers the TMA paths (L % 32 == 0), the generic fallbacks (ragged L), every
+dW scheme and both multiply-add modes, and checks results against the oracle
+so a sanitizer-clean run is also a correct run.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2604_25422_b200 as ks  # noqa: E402
+from oracle.oracle import CHUNKED, PAIRWISE, SEQUENTIAL, Oracle  # noqa: E402
+
+o = Oracle()
+shapes = [(2, 3, 4096, 7), (2, 2, 1024, 64), (1, 2, 2048, 256), (2, 2, 1000, 5), (1, 1, 96, 40)]
+for (B, H, L, K) in shapes:
+    x, k, gy = o.fill_inputs(3, B, H, L, K)
+    dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
+    for mode in (0, 1):
+        y = ks.forward(dx_, dk_, mode)
+        d = ks.backward_input(dgy, dk_, mode)
+        torch.cuda.synchronize()
+        assert np.array_equal(y.cpu().numpy(), o.forward(x, k, mode))
+        assert np.array_equal(d.cpu().numpy(), o.backward_input(gy, k, mode))
+        for s, c in ((ks.HIERARCHICAL, 0), (PAIRWISE, 0), (CHUNKED, 300), (SEQUENTIAL, 0)):
+            if s == SEQUENTIAL and B * L > 5000:
+                continue
+            dk = ks.backward_weight(dgy, dx_, K, s, c, mode)
+            torch.cuda.synchronize()
+            if s != ks.HIERARCHICAL:
+                assert np.array_equal(dk.cpu().numpy(), o.backward_weight(gy, x, K, s, c, mode))
+    yh, dxh, dkh = ks.step_host(x, k, gy, scheme=ks.HIERARCHICAL, mode=1)
+print("sanitize cases ok")
