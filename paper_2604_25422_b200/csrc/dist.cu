@@ -121,7 +121,7 @@ ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm*
     if (!dk || !comm) return KS_ERR_NULL;
     if (H < 1) return KS_ERR_DIM_H;
     if (K < 1) return KS_ERR_DIM_K;
-    if (comm->world == 1) return KS_OK;
+    // (a 1-rank communicator still goes through NCCL: same code path at every N)
     return nccl_status(ncclAllReduce(dk, dk, static_cast<size_t>(H * K), ncclFloat, ncclSum,
                                      comm->nccl, static_cast<cudaStream_t>(stream)));
 }
@@ -132,7 +132,6 @@ ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, 
     if (H < 1) return KS_ERR_DIM_H;
     if (K < 1) return KS_ERR_DIM_K;
     if (comm->world > 64) return KS_ERR_SHARD;
-    if (comm->world == 1) return KS_OK;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t n = static_cast<size_t>(H * K);
     ks_status s = nccl_status(ncclAllGather(dk, gather, n, ncclFloat, comm->nccl, st));

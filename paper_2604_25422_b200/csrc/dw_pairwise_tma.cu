@@ -198,8 +198,10 @@ dw_pairwise_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constan
         const unsigned char* xs = gys + g.gy_bytes;
         const int t0 = (u % ntt) * kTT;
         float node[kJR];
-        // every x tap of the item inside the row -> no leaf masking needed
-        const bool interior = t0 + jbase >= 0 && t0 + kTT - 1 + jbase + kJR - 1 < L;
+        // every x tap of this lane's leaves inside the row -> no leaf masking
+        // (only the lanes at a row's two ends take the masked path)
+        const int lt = t0 + static_cast<int>(seg_t);
+        const bool interior = lt + jbase >= 0 && lt + 8 * NB - 1 + jbase + kJR - 1 < L;
         if (interior)
             seg_tree<NB, S, false>(gys, xs, seg_t, 0, A, jg * kJR, t0, jbase, L, node);
         else

@@ -277,6 +277,12 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     const int s = static_cast<int>((4 - off % 4) % 4);
     int NS = 4;
     while (NS > 2 && stencil_smem_bytes(g, NS, tma_out) > 110 * 1024) --NS;
+    if (R == 32) {
+        // compute-bound: spend shared memory on resident warps rather than deep
+        // prefetch.  With K >= 1024 a tile's FMAs (R*K per thread) outlast its
+        // load by ~100x and one stage suffices; shorter K keeps one tile in flight.
+        NS = K >= 1024 ? 1 : 2;
+    }
     if (stencil_smem_bytes(g, NS, tma_out) > 220 * 1024) return KS_OK;
 
     float* kp = nullptr;

@@ -266,3 +266,22 @@ def test_reference_unit_tests_against_dropin():
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "21 | 21 passed" in r.stdout
+
+
+def test_nccl_combine_single_rank():
+    """The C library's own NCCL communicator on this GPU (world size 1 -- the
+    round's boxes have one GPU; N > 1 is covered by tests/test_dist_gloo.py):
+    allreduce and the fixed-order allgather combine leave dk bit-unchanged."""
+    B, H, L, K = 4, 8, 2048, 7
+    x, k, gy = ks.make_inputs(5, B, H, L, K)
+    dk = ks.backward_weight(gy, x, K, PAIRWISE)
+    ref = host(dk).copy()
+    comm = ks.Comm(ks.Comm.unique_id(), 1, 0)
+    try:
+        comm.allreduce_dw(dk)
+        assert same(host(dk), ref)
+        gather = torch.empty((1, H, K), dtype=torch.float32, device="cuda")
+        comm.allgather_sum_dw(dk, gather)
+        assert same(host(dk), ref)
+    finally:
+        comm.close()
