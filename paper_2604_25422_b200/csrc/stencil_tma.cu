@@ -21,6 +21,7 @@
 // buffered), compute-bound shapes (long K, R = 32) store 128-bit streaming
 // writes straight from registers and spend the shared memory on occupancy.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
@@ -220,6 +221,11 @@ ks_status launch_s(int s, bool fused, const CUtensorMap& im, const CUtensorMap& 
 
 }  // namespace
 
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
 // Register-tile shape for (L, K): R = 32 for compute-bound long K, R = 16 for
 // memory-bound short K, R = 4 for short rows; NT chosen so a tile (NT*R
 // outputs) does not exceed the row.
@@ -245,6 +251,10 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
     int R, NT;
     pick_tile(L, K, &R, &NT);
+    if (R == 16 && env_int("KS_STENCIL_NT", 0) > 0) {  // tuning knob (bench sweeps)
+        const int nt = env_int("KS_STENCIL_NT", 0);
+        if ((nt == 64 || nt == 128 || nt == 256) && nt * R <= L) NT = nt;
+    }
     const bool tma_out = R != 32;
     StencilGeom g;
     g.T = NT * R;
@@ -277,6 +287,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     const int s = static_cast<int>((4 - off % 4) % 4);
     int NS = 4;
     while (NS > 2 && stencil_smem_bytes(g, NS, tma_out) > 110 * 1024) --NS;
+    if (env_int("KS_STENCIL_NS", 0) > 0) NS = std::min(8, env_int("KS_STENCIL_NS", 0));  // tuning knob
     if (R == 32) {
         // compute-bound: spend shared memory on resident warps rather than deep
         // prefetch.  With K >= 1024 a tile's FMAs (R*K per thread) outlast its
