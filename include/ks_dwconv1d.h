@@ -145,6 +145,26 @@ ks_status ks_dwconv1d_step_f32_host(const float* x, const float* k, const float*
                                     float* dk, int64_t B, int64_t H, int64_t L, int64_t K, int scheme,
                                     int64_t chunk, int mode);
 
+/* ---- the paper's four kernel designs (ablation) -------- */
+/* Real sm_100a kernels with the launch geometry and thread mapping of the
+ * reference's analytical model (src/exec_model.cpp:80-135): variant 0 naive,
+ * 1 coalesced (TTILE=32, HTILE=8), 2 shared (TPB=256 halo tile), 3 warp-tiled;
+ * path 0 forward (a=x, b=k), 1 dX (a=gy, b=k), 2 dW (a=gy, b=x; out=[H,K]).
+ * fwd/dX are bit-identical to the reference; naive dW = SEQUENTIAL.  Returns
+ * KS_ERR_SHARD when the literal mapping cannot launch this shape (grid
+ * limits, a row or chunk that does not fit shared memory), KS_ERR_BAD_SCHEME
+ * for an unknown variant or path. */
+typedef enum ks_variant {
+    KS_VARIANT_NAIVE = 0,
+    KS_VARIANT_COALESCED = 1,
+    KS_VARIANT_SHARED = 2,
+    KS_VARIANT_WARP = 3
+} ks_variant;
+ks_status ks_dwconv1d_variant_workspace_bytes(int variant, int path, int64_t H, int64_t K, size_t* bytes);
+ks_status ks_dwconv1d_variant_f32(int variant, int path, const float* a, const float* b, float* out,
+                                  int64_t B, int64_t H, int64_t L, int64_t K, int mode, void* ws,
+                                  size_t ws_bytes, void* stream);
+
 /* ---- batch sharding across GPUs (one process per GPU) --------------------- */
 /* Contiguous batch slice of rank `rank` out of `world`: rows [*b0, *b0+*nb).
  * Slices differ by at most one row; pure host arithmetic (no device). */

@@ -33,6 +33,7 @@ EXPORTED = [
     "ks_dwconv1d_fwd_f32_host", "ks_dwconv1d_dx_f32_host", "ks_dwconv1d_dw_f32_host",
     "ks_dwconv1d_fwd_f64_host", "ks_dwconv1d_dx_f64_host", "ks_dwconv1d_dw_f64_host",
     "ks_dwconv1d_step_f32_host",
+    "ks_dwconv1d_variant_workspace_bytes", "ks_dwconv1d_variant_f32",
     "ks_shard_rows", "ks_comm_unique_id", "ks_comm_init", "ks_comm_destroy",
     "ks_dwconv1d_dw_allreduce_f32", "ks_dwconv1d_dw_allgather_sum_f32",
 ]
@@ -57,6 +58,8 @@ _SIGS = {
     "ks_dwconv1d_dx_f64_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int], _int),
     "ks_dwconv1d_dw_f64_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _i64, _int], _int),
     "ks_dwconv1d_step_f32_host": ([_p] * 6 + [_i64, _i64, _i64, _i64, _int, _i64, _int], _int),
+    "ks_dwconv1d_variant_workspace_bytes": ([_int, _int, _i64, _i64, C.POINTER(_sz)], _int),
+    "ks_dwconv1d_variant_f32": ([_int, _int, _p, _p, _p, _i64, _i64, _i64, _i64, _int, _p, _sz, _p], _int),
     "ks_shard_rows": ([_i64, _int, _int, C.POINTER(_i64), C.POINTER(_i64)], _int),
     "ks_comm_unique_id": ([_p], _int),
     "ks_comm_init": ([C.POINTER(_p), _p, _int, _int], _int),

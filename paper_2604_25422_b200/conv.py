@@ -179,6 +179,31 @@ def step_host(x, k, gy, K: int | None = None, scheme: int = HIERARCHICAL, chunk:
     return y, dx, dk
 
 
+VARIANTS = {"naive": 0, "coalesced": 1, "shared": 2, "warp": 3}
+PATHS = {"fwd": 0, "dx": 1, "dw": 2}
+
+
+def variant(name: str, path: str, a, b, K: int | None = None, mode: int = FUSED, out=None):
+    """Run one of the paper's four kernel designs on device
+    tensors: path 'fwd' (a=x, b=k), 'dx' (a=gy, b=k) or 'dw' (a=gy, b=x, K)."""
+    v, p = VARIANTS[name], PATHS[path]
+    B, H, L = _dims3(a, f"{name} {path}: a")
+    if p == 2:
+        _dims3(b, f"{name} dw: x", (B, H, L))
+        if K is None:
+            raise ValueError("dw needs K")
+        shape_out = (H, K)
+    else:
+        K = _dims_k(b, f"{name} {path}: k", H)
+        shape_out = (B, H, L)
+    if out is None:
+        out = _empty_like(a, shape_out)
+    st = _lib.lib().ks_dwconv1d_variant_f32(v, p, _ptr(a), _ptr(b), _ptr(out), B, H, L, K, mode, None, 0,
+                                           _stream(a))
+    _raise_dims(st, f"variant {name} {path}")
+    return out
+
+
 def fill_pm1(seed: int, first: int, out) -> None:
     """Device splitmix64 fill, bit-identical to the reference SplitMix64 stream
     (include/kernelscope/rng.hpp:12-28): out.flat[i] = draw first+1+i."""

@@ -19,6 +19,11 @@ ks_status dw_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, 
 ks_status dw_f64(const double*, const double*, double*, int64_t, int64_t, int64_t, int64_t, int,
                  int64_t, int, void*, cudaStream_t);
 
+size_t variant_workspace_bytes(int variant, int path, int64_t H, int64_t K);
+bool variant_supported(int variant, int path, int64_t B, int64_t H, int64_t L, int64_t K);
+ks_status variant_f32(int variant, int path, const float* a, const float* b, float* out, int64_t B, int64_t H,
+                      int64_t L, int64_t K, int mode, void* ws, cudaStream_t st);
+
 static thread_local std::string g_last_error;
 
 void set_last_error(const char* what) { g_last_error = what ? what : ""; }
@@ -206,6 +211,30 @@ ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int6
     Scratch s;
     KS_TRY(s.take(ws, ws_bytes, dw_workspace_bytes(B, H, L, K, scheme, chunk, 8), st));
     return dw_f64(gy, x, dk, B, H, L, K, scheme, chunk, mode, s.ptr, st);
+}
+
+ks_status ks_dwconv1d_variant_workspace_bytes(int variant, int path, int64_t H, int64_t K, size_t* bytes) {
+    if (!bytes) return KS_ERR_NULL;
+    if (variant < 0 || variant > 3 || path < 0 || path > 2) return KS_ERR_BAD_SCHEME;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (K < 1) return KS_ERR_DIM_K;
+    *bytes = variant_workspace_bytes(variant, path, H, K);
+    return KS_OK;
+}
+
+ks_status ks_dwconv1d_variant_f32(int variant, int path, const float* a, const float* b, float* out, int64_t B,
+                                  int64_t H, int64_t L, int64_t K, int mode, void* ws, size_t ws_bytes,
+                                  void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (variant < 0 || variant > 3 || path < 0 || path > 2) return KS_ERR_BAD_SCHEME;
+    if (!a || !b || !out) return KS_ERR_NULL;
+    if (!variant_supported(variant, path, B, H, L, K)) return KS_ERR_SHARD;
+    KS_TRY(check_device());
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch s;
+    KS_TRY(s.take(ws, ws_bytes, variant_workspace_bytes(variant, path, H, K), st));
+    return variant_f32(variant, path, a, b, out, B, H, L, K, mode, s.ptr, st);
 }
 
 ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream) {

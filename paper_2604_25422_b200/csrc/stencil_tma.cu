@@ -285,7 +285,9 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     if (tma_out && !encode_row_view(&om, out, B * H, L, kIn, g.MR, sw)) return KS_OK;
     if (!tma_out) om = im;  // unused
     const int s = static_cast<int>((4 - off % 4) % 4);
-    int NS = 4;
+    // memory-bound tiles: 3 stages x 2 CTAs/SM measured best on config 3 (a
+    // sweep of NT in {128,256} x NS in {2,3,4,6,8} spans 5.9-6.3 TB/s)
+    int NS = 3;
     while (NS > 2 && stencil_smem_bytes(g, NS, tma_out) > 110 * 1024) --NS;
     if (env_int("KS_STENCIL_NS", 0) > 0) NS = std::min(8, env_int("KS_STENCIL_NS", 0));  // tuning knob
     if (R == 32) {

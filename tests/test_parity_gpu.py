@@ -87,6 +87,24 @@ def test_dw_pairwise_fast_path_bitwise(oracle, shape):
     assert same(got0, oracle.backward_weight(z, x, K, PAIRWISE))
 
 
+@pytest.mark.parametrize("name", ["naive", "coalesced", "shared", "warp"])
+@pytest.mark.parametrize("shape", [(3, 5, 48, 48), (2, 9, 100, 7), (2, 3, 1030, 64), (1, 2, 257, 300)])
+def test_paper_variants(oracle, name, shape):
+    """The paper's four kernel designs: fwd/dX bitwise,
+    naive dW = the Sequential scheme bitwise, two-stage dW within tolerance."""
+    B, H, L, K = shape
+    x, k, gy = oracle.fill_inputs(11, B, H, L, K)
+    for m in (SEPARATE, FUSED):
+        assert same(host(ks.variant(name, "fwd", dev(x), dev(k), mode=m)), oracle.forward(x, k, m))
+        assert same(host(ks.variant(name, "dx", dev(gy), dev(k), mode=m)), oracle.backward_input(gy, k, m))
+        dk = host(ks.variant(name, "dw", dev(gy), dev(x), K, mode=m))
+        if name == "naive":
+            assert same(dk, oracle.backward_weight(gy, x, K, SEQUENTIAL, 0, m))
+        else:
+            truth = oracle.backward_weight(gy.astype(np.float64), x.astype(np.float64), K, PAIRWISE)
+            assert normwise(dk, truth) <= HIER_TOL
+
+
 @pytest.mark.parametrize("shape", SHAPES)
 def test_dw_hierarchical_tolerance(oracle, shape):
     B, H, L, K = shape
