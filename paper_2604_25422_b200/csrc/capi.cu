@@ -3,7 +3,9 @@
 // shape.hpp:27-31; chunk_size >= 1, src/conv_core.cpp:154-156), launch
 // selection, scratch management and the on-device splitmix64 generator.
 #include <cstring>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "ks_common.cuh"
 
@@ -36,6 +38,76 @@ ks_status cuda_status(cudaError_t e) {
 }
 
 ks_status check_launch() { return cuda_status(cudaGetLastError()); }
+
+static cudaMemPool_t scratch_pool() {
+    constexpr int kMaxDev = 64;
+    static cudaMemPool_t pools[kMaxDev] = {};
+    static bool made[kMaxDev] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= kMaxDev) return nullptr;
+    if (!made[dev]) {
+        made[dev] = true;
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.handleTypes = cudaMemHandleTypeNone;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) == cudaSuccess) {
+            uint64_t thr = ~0ull;
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            pools[dev] = nullptr;
+            cudaGetLastError();
+        }
+    }
+    return pools[dev];
+}
+
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaMemPool_t pool = scratch_pool();
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
+
+void scratch_free(void* p, cudaStream_t st) { cudaFreeAsync(p, st); }
+
+int prepare_kernel(const void* func, int threads, int smem) {
+    // The dynamic-smem opt-in is per (kernel, device) and only ever raised, so a
+    // later smaller request never lowers the limit under a larger cached one.
+    struct Limit {
+        const void* func;
+        int dev, smem;
+    };
+    struct Occ {
+        const void* func;
+        int dev, threads, smem, per_sm;
+    };
+    static std::mutex mu;
+    static std::vector<Limit> limits;
+    static std::vector<Occ> occ;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> g(mu);
+    Limit* lim = nullptr;
+    for (Limit& l : limits)
+        if (l.func == func && l.dev == dev) lim = &l;
+    if (!lim) {
+        limits.push_back({func, dev, 0});
+        lim = &limits.back();
+    }
+    if (smem > lim->smem) {
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        lim->smem = smem;
+    }
+    for (const Occ& o : occ)
+        if (o.func == func && o.dev == dev && o.threads == threads && o.smem == smem) return o.per_sm;
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, func, threads, smem);
+    if (per_sm < 1) per_sm = 1;
+    if (occ.size() > 4096) occ.clear();
+    occ.push_back({func, dev, threads, smem, per_sm});
+    return per_sm;
+}
 
 static ks_status check_shape(int64_t B, int64_t H, int64_t L, int64_t K) {
     if (B < 1) return KS_ERR_DIM_B;
@@ -101,10 +173,10 @@ struct Scratch {
             return KS_OK;
         }
         owned = true;
-        return cuda_status(cudaMallocAsync(&ptr, need, s));
+        return cuda_status(scratch_alloc(&ptr, need, s));
     }
     ~Scratch() {
-        if (owned && ptr) cudaFreeAsync(ptr, st);
+        if (owned && ptr) scratch_free(ptr, st);
     }
 };
 

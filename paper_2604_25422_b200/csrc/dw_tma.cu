@@ -180,7 +180,7 @@ ks_status launch(int s, const CUtensorMap& gm, const CUtensorMap& xm, const CUte
 #define KS_DW_CASE(SV)                                                                                        \
     case SV: {                                                                                                \
         auto kern = dw_tma<JR, TB, NJ, SV, FUSED>;                                                            \
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);                        \
+        prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                \
         kern<<<blocks, kThreads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),      \
                                              static_cast<int>(L), static_cast<int>(K), p, G, NJT, g, NS);     \
         break;                                                                                                \

@@ -52,6 +52,18 @@ inline int num_sms() {
     return n;
 }
 
+// Stream-ordered scratch from a library-owned memory pool (one per device,
+// release threshold = unlimited): freed blocks stay cached across stream
+// synchronisations, so a call after a sync does not re-map memory, and the
+// process-wide default pool is left untouched.
+cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st);
+void scratch_free(void* p, cudaStream_t st);
+
+// Opts `func` in to `smem` bytes of dynamic shared memory on the current device
+// and returns its resident CTAs per SM, caching both per (device, kernel,
+// smem, threads) so the per-call host cost is a table lookup.
+int prepare_kernel(const void* func, int threads, int smem);
+
 // Records a CUDA error for ks_last_error_string and maps it to a status.
 ks_status cuda_status(cudaError_t e);
 ks_status check_launch();

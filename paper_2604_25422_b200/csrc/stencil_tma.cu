@@ -29,6 +29,8 @@
 namespace ks {
 
 __global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int);
+ks_status stencil_cb_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
+                         int64_t off, int reverse, int mode, cudaStream_t st, bool* handled);
 
 namespace {
 
@@ -190,10 +192,7 @@ ks_status launch(const CUtensorMap& im, const CUtensorMap& om, const float* kp, 
     constexpr bool TMA_OUT = R != 32;
     auto kern = stencil_tma<R, NT, S, FUSED, TMA_OUT>;
     const int smem = stencil_smem_bytes(g, NS, TMA_OUT);
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, smem);
-    if (per_sm < 1) per_sm = 1;
+    const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), NT, smem);
     const int tiles_per_row = static_cast<int>((L + g.T - 1) / g.T);
     const int ntiles = static_cast<int>(B * H * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
@@ -249,6 +248,10 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     *handled = false;
     if (L % kIn != 0 || L >= (int64_t(1) << 30) || K > 8192) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
+    if (env_int("KS_STENCIL_CB", 1)) {  // compute-bound long-K kernel (stencil_cb.cu)
+        const ks_status s = stencil_cb_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
+        if (*handled) return s;
+    }
     int R, NT;
     pick_tile(L, K, &R, &NT);
     if (R == 16 && env_int("KS_STENCIL_NT", 0) > 0) {  // tuning knob (bench sweeps)
@@ -299,7 +302,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     if (stencil_smem_bytes(g, NS, tma_out) > 220 * 1024) return KS_OK;
 
     float* kp = nullptr;
-    ks_status rc = cuda_status(cudaMallocAsync(&kp, sizeof(float) * H * g.Kp, st));
+    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
     if (rc != KS_OK) return rc;
     prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
         k, kp, H, K, g.Kp, reverse);
@@ -314,7 +317,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
         else if (NT == 128) rc = launch_s<32, 128>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
         else rc = launch_s<32, 64>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
     }
-    cudaFreeAsync(kp, st);
+    scratch_free(kp, st);
     *handled = true;
     return rc;
 }
