@@ -473,6 +473,9 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
 ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
                         cudaStream_t, bool*);
 
+ks_status dw_rows_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
+                         cudaStream_t, bool*);
+
 ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                  int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
     if (scheme == KS_DW_PAIRWISE && !tma_disabled()) {
@@ -488,7 +491,8 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
     float* part = static_cast<float*>(ws);
     bool handled = false;
     ks_status s = KS_OK;
-    if (!tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
+    if (L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
+    if (!handled && !tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
     if (!handled)
         s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
                                     : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);

@@ -217,6 +217,8 @@ static ks_status launch_direct(const T* in, const T* k, T* out, int64_t B, int64
 
 ks_status stencil_tma_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
                           int, int, cudaStream_t, bool*);
+ks_status stencil_rows_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
+                           int, int, cudaStream_t, bool*);
 
 bool tma_disabled() {
     static const bool off = [] {
@@ -230,6 +232,11 @@ bool tma_disabled() {
 ks_status conv_stencil_f32(const float* in, const float* k, float* out, int64_t B, int64_t H,
                            int64_t L, int64_t K, int64_t off, int reverse, int mode,
                            cudaStream_t st) {
+    if (L < 1024) {  // short rows: whole rows per CTA (rows_short.cu)
+        bool handled = false;
+        const ks_status s = stencil_rows_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
+        if (handled) return s;
+    }
     if (!tma_disabled()) {
         bool handled = false;
         const ks_status s = stencil_tma_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
