@@ -418,13 +418,23 @@ size_t dw_pairwise_tma_workspace(int64_t B, int64_t H, int64_t L, int64_t K);
 ks_status dw_pairwise_tma_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                               int64_t K, void* ws, cudaStream_t st, bool* handled);
 bool tma_disabled();
+bool dw_cb_applies(int64_t B, int64_t H, int64_t L, int64_t K);
+int dw_cb_groups(int64_t B, int64_t H, int64_t K);
+ks_status dw_cb_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+                       int G, int mode, cudaStream_t st, bool* handled);
+
+// Row groups G of the HIERARCHICAL partial buffer part[G,H,K] for this shape.
+static int hier_groups(int64_t B, int64_t H, int64_t L, int64_t K) {
+    if (!tma_disabled() && dw_cb_applies(B, H, L, K)) return dw_cb_groups(B, H, K);
+    return hier_plan(B, H, K).g;
+}
 
 size_t dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                           int elem) {
     if (scheme == KS_DW_HIERARCHICAL) {
         if (elem != 4) return 0;  // fp64 HIERARCHICAL runs the exact pairwise kernel
-        const HierPlan pl = hier_plan(B, H, K);
-        return size_t(pl.g) * H * K * sizeof(float);
+        const int g = std::max(hier_groups(B, H, L, K), hier_plan(B, H, K).g);
+        return size_t(g) * H * K * sizeof(float);
     }
     if (scheme == KS_DW_PAIRWISE) return elem == 4 ? dw_pairwise_tma_workspace(B, H, L, K) : 0;
     const int64_t nc = chunk_count(B, L, scheme, chunk);
@@ -487,11 +497,16 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
         return dw_exact<float>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);
     if (L > (1ll << 30) || K > (1ll << 30) || B > (1ll << 30))
         return dw_exact<float>(gy, x, dk, B, H, L, K, KS_DW_PAIRWISE, 0, mode, ws, st);
-    const HierPlan pl = hier_plan(B, H, K);
+    HierPlan pl = hier_plan(B, H, K);
     float* part = static_cast<float*>(ws);
     bool handled = false;
     ks_status s = KS_OK;
-    if (L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
+    if (!tma_disabled() && dw_cb_applies(B, H, L, K)) {  // compute-bound long K (dw_cb.cu)
+        pl.g = dw_cb_groups(B, H, K);
+        s = dw_cb_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
+        if (!handled) pl = hier_plan(B, H, K);
+    }
+    if (!handled && L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
     if (!handled && !tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
     if (!handled)
         s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
