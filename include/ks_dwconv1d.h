@@ -118,6 +118,10 @@ ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int6
  * fill(seed,B*H*L), gy = fill(seed,B*H*L+H*K). */
 ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream);
 
+/* Measured FP32 FMA throughput of the current device (TFLOP/s, 2 FLOP per
+ * FMA): the compute roof for the long-K (FP32-bound) shapes.  Synchronous. */
+ks_status ks_probe_fp32_tflops(double* tflops);
+
 /* ---- host-buffer entry points (synchronous; the value-type API shape) ---- */
 /* Inputs/outputs are host pointers (pinned or pageable).  The call streams
  * row blocks host->device, runs the kernels and streams results back with

@@ -159,6 +159,24 @@ __global__ void fill_pm1_kernel(uint64_t seed, uint64_t first, float* __restrict
     }
 }
 
+// FP32 FMA throughput probe (the compute roof of the long-K configs): 8
+// independent FMA chains per thread, enough CTAs for every SM.
+__global__ void __launch_bounds__(256) fp32_peak_probe(float* out, int iters, float b, float c) {
+    float a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = threadIdx.x * 1e-3f + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r)
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = __fmaf_rn(a[i], b, c);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += a[i];
+    if (s == 12345.f) out[0] = s;  // keeps the chains alive
+}
+
 // Scratch for dW: caller-provided, or stream-ordered from the device pool.
 struct Scratch {
     void* ptr = nullptr;
@@ -307,6 +325,31 @@ ks_status ks_dwconv1d_variant_f32(int variant, int path, const float* a, const f
     Scratch s;
     KS_TRY(s.take(ws, ws_bytes, variant_workspace_bytes(variant, path, H, K), st));
     return variant_f32(variant, path, a, b, out, B, H, L, K, mode, s.ptr, st);
+}
+
+ks_status ks_probe_fp32_tflops(double* tflops) {
+    if (!tflops) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    float* out = nullptr;
+    KS_TRY(cuda_status(cudaMalloc(&out, sizeof(float))));
+    const int blocks = num_sms() * 8, iters = 4096;
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    fp32_peak_probe<<<blocks, 256>>>(out, 64, 0.999f, 1e-4f);  // warm-up (clocks up)
+    cudaEventRecord(a);
+    fp32_peak_probe<<<blocks, 256>>>(out, iters, 0.999f, 1e-4f);
+    cudaEventRecord(b);
+    ks_status s = cuda_status(cudaEventSynchronize(b));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(out);
+    if (s != KS_OK) return s;
+    const double fma = double(blocks) * 256 * iters * 16 * 8;
+    *tflops = 2.0 * fma / (ms * 1e-3) / 1e12;
+    return KS_OK;
 }
 
 ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream) {
