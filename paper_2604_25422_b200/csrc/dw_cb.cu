@@ -190,7 +190,10 @@ ks_status dw_cb_stage1(const float* gy, const float* x, float* part, int64_t B, 
     const int nts = kNT / njg;
     DwCbGeom g;
     g.JT = njg * kJR;
-    g.TT = std::max(32 * nts, 2048);
+    // t per work item: >= 2 chunks of 32 per thread (amortises the re-layout),
+    // capped by the row
+    g.TT = std::min<int64_t>(std::max(64 * nts, 4096), (L + 31) / 32 * 32);
+    g.TT = std::max(g.TT, 32 * nts);
     const int njt = static_cast<int>((K + g.JT - 1) / g.JT);
     if (int64_t(G) * H * njt >= (int64_t(1) << 31)) return KS_OK;
     g.XW = (g.TT + g.JT + 32 + 31) / 32 * 32 + 32;  // window + the D shift + read overrun
