@@ -246,11 +246,13 @@ def run_ours(args, cfg_name, cfg):
     mode = ks.FUSED if args.mode == "fused" else ks.SEPARATE
     scheme = {"hierarchical": ks.HIERARCHICAL, "pairwise": ks.PAIRWISE}[args.scheme]
 
-    comm = None
+    comm = peer = None
     if world > 1:
         uid = [ks.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = ks.Comm(uid[0], world, rank)
+        if args.combine == "peer" and scheme == ks.HIERARCHICAL:
+            peer = comm.peer(B, H, L, K)  # NVLink peer-memory combine fused into dW
 
     # inputs: rows [rank*B, rank*B+B) of the (B*world)-row problem, generated in place
     x, k, gy = ks.make_inputs(args.seed, B, H, L, K, device=dev, b0=rank * B, B_total=B * world)
@@ -270,10 +272,13 @@ def run_ours(args, cfg_name, cfg):
         ks.backward_input(gy, k, mode, out=dx)
         if ev:
             ev[2].record(stream)
-        ks.backward_weight(gy, x, K, scheme, 0, mode, out=dk, workspace=ws)
+        if peer is not None:  # stage 1 + fused signal/wait/combine over peer memory
+            peer.backward_weight(gy, x, K, mode, out=dk)
+        else:
+            ks.backward_weight(gy, x, K, scheme, 0, mode, out=dk, workspace=ws)
         if ev:
             ev[3].record(stream)
-        if comm is not None:
+        if comm is not None and peer is None:
             comm.allreduce_dw(dk)
         if ev:
             ev[4].record(stream)
@@ -430,7 +435,9 @@ def run_ours(args, cfg_name, cfg):
             "data": "synthetic (reference splitmix64 stream, generated on device)",
             "config": {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B_per_gpu": B, "H": H,
                        "L": L, "K": K, "global_batch": B * world,
-                       "parallelism": f"batch-shard dp{world}" + (" + NCCL dW allreduce" if world > 1 else ""),
+                       "parallelism": f"batch-shard dp{world}" + (
+                           "" if world == 1 else " + dW combine fused over NVLink peer memory" if peer is not None
+                           else " + NCCL dW allreduce"),
                        "mode": args.mode, "dw_scheme": args.scheme,
                        "l2": "inputs larger than L2 (no flush)" if 4 * B * H * L > 2 * 126e6
                              else "working set fits L2 (not flushed)"},
@@ -439,6 +446,8 @@ def run_ours(args, cfg_name, cfg):
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
+    if peer is not None:
+        peer.close()
     if comm is not None:
         comm.close()
     if world > 1:
@@ -455,6 +464,8 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default="config3")
     ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
     ap.add_argument("--scheme", choices=["hierarchical", "pairwise"], default="hierarchical")
+    ap.add_argument("--combine", choices=["nccl", "peer"], default="nccl",
+                    help="N>1 dW combine: one ncclAllReduce, or the fused NVLink peer-memory kernel")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--e2e-path", choices=["step", "calls"], default="step")

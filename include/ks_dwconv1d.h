@@ -189,6 +189,23 @@ ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm*
 ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, int64_t K,
                                            ks_comm* comm, void* stream);
 
+/* ---- dW with the cross-GPU combine fused into the reduction (NVLink) ----- */
+/* The dW step of a batch-sharded training step is a compute step followed by
+ * a collective.  ks_peer exposes each rank's partial buffer to every peer via
+ * CUDA IPC (mapped over NVLink/NVSwitch; handles exchanged once through the
+ * NCCL communicator); ks_dwconv1d_dw_f32_peer then runs the HIERARCHICAL
+ * stage 1 into it and ONE kernel that signals the peers, waits for them
+ * (system-scope release/acquire flags) and sums every rank's partials straight
+ * from peer memory in fixed (rank, group) order -- identical bits on every
+ * rank, no NCCL call on the data path.  Collective: every rank must call it. */
+typedef struct ks_peer ks_peer;
+ks_status ks_peer_create(ks_comm* comm, size_t partial_bytes, ks_peer** peer);
+ks_status ks_peer_destroy(ks_peer* peer);
+ks_status ks_dwconv1d_dw_f32_peer(const float* gy, const float* x, float* dk, int64_t B, int64_t H,
+                                  int64_t L, int64_t K, int mode, ks_peer* peer, void* stream);
+/* 1 when a combine gave up waiting (~10 s) for a peer that never arrived. */
+ks_status ks_peer_timed_out(ks_peer* peer, int* flag);
+
 #ifdef __cplusplus
 }
 #endif

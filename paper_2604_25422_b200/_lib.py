@@ -36,6 +36,7 @@ EXPORTED = [
     "ks_dwconv1d_variant_workspace_bytes", "ks_dwconv1d_variant_f32",
     "ks_shard_rows", "ks_comm_unique_id", "ks_comm_init", "ks_comm_destroy",
     "ks_dwconv1d_dw_allreduce_f32", "ks_dwconv1d_dw_allgather_sum_f32",
+    "ks_peer_create", "ks_peer_destroy", "ks_dwconv1d_dw_f32_peer", "ks_peer_timed_out",
 ]
 
 _i64, _u64, _p, _int, _sz = C.c_int64, C.c_uint64, C.c_void_p, C.c_int, C.c_size_t
@@ -67,6 +68,10 @@ _SIGS = {
     "ks_comm_destroy": ([_p], _int),
     "ks_dwconv1d_dw_allreduce_f32": ([_p, _i64, _i64, _p, _p], _int),
     "ks_dwconv1d_dw_allgather_sum_f32": ([_p, _p, _i64, _i64, _p, _p], _int),
+    "ks_peer_create": ([_p, _sz, C.POINTER(_p)], _int),
+    "ks_peer_destroy": ([_p], _int),
+    "ks_dwconv1d_dw_f32_peer": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _p, _p], _int),
+    "ks_peer_timed_out": ([_p, C.POINTER(_int)], _int),
 }
 
 _lib = None

@@ -265,7 +265,41 @@ class Comm:
                                                           self.handle, _stream(dk)),
               "dw_allgather_sum")
 
+    def peer(self, B: int, H: int, L: int, K: int) -> "Peer":
+        """NVLink peer-memory dW combine for per-rank shape (B,H,L,K)."""
+        return Peer(self, workspace_bytes(B, H, L, K, HIERARCHICAL))
+
     def close(self) -> None:
         if self.handle:
             _lib.lib().ks_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+
+class Peer:
+    """ks_peer: dW whose cross-rank sum is fused into the reduction kernel and
+    read straight from the peers' memory (no NCCL on the data path)."""
+
+    def __init__(self, comm: Comm, partial_bytes: int):
+        self.handle = C.c_void_p()
+        check(_lib.lib().ks_peer_create(comm.handle, max(partial_bytes, 4), C.byref(self.handle)),
+              "peer_create")
+
+    def backward_weight(self, gy, x, K: int, mode: int = FUSED, out=None):
+        B, H, L = _dims3(gy, "peer dw: gy")
+        _dims3(x, "peer dw: x", (B, H, L))
+        if out is None:
+            out = _empty_like(gy, (H, K))
+        st = _lib.lib().ks_dwconv1d_dw_f32_peer(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, mode,
+                                               self.handle, _stream(gy))
+        _raise_dims(st, "dw_peer")
+        return out
+
+    def timed_out(self) -> bool:
+        f = C.c_int(0)
+        check(_lib.lib().ks_peer_timed_out(self.handle, C.byref(f)), "peer_timed_out")
+        return bool(f.value)
+
+    def close(self) -> None:
+        if self.handle:
+            _lib.lib().ks_peer_destroy(self.handle)
             self.handle = C.c_void_p()

@@ -485,6 +485,8 @@ ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, in
 
 ks_status dw_rows_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
                          cudaStream_t, bool*);
+ks_status dw_stage1_only(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, void*, int*,
+                         cudaStream_t);
 
 ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                  int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
@@ -497,8 +499,20 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
         return dw_exact<float>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);
     if (L > (1ll << 30) || K > (1ll << 30) || B > (1ll << 30))
         return dw_exact<float>(gy, x, dk, B, H, L, K, KS_DW_PAIRWISE, 0, mode, ws, st);
-    HierPlan pl = hier_plan(B, H, K);
     float* part = static_cast<float*>(ws);
+    int G = 0;
+    ks_status s = dw_stage1_only(gy, x, part, B, H, L, K, mode, nullptr, &G, st);
+    if (s != KS_OK) return s;
+    const int64_t HK = H * K;
+    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, G);
+    return check_launch();
+}
+
+// HIERARCHICAL stage 1 only: per-CTA partials part[G,H,K] (G returned), for
+// the fused cross-GPU combine of peer.cu and for dw_f32 above.
+ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+                         int mode, void*, int* G, cudaStream_t st) {
+    HierPlan pl = hier_plan(B, H, K);
     bool handled = false;
     ks_status s = KS_OK;
     if (!tma_disabled() && dw_cb_applies(B, H, L, K)) {  // compute-bound long K (dw_cb.cu)
@@ -511,10 +525,8 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
     if (!handled)
         s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
                                     : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);
-    if (s != KS_OK) return s;
-    const int64_t HK = H * K;
-    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.g);
-    return check_launch();
+    *G = pl.g;
+    return s;
 }
 
 ks_status dw_f64(const double* gy, const double* x, double* dk, int64_t B, int64_t H, int64_t L,

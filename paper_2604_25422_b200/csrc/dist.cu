@@ -12,12 +12,7 @@
 #include <nccl.h>
 
 #include "ks_common.cuh"
-
-struct ks_comm {
-    ncclComm_t nccl = nullptr;
-    int world = 1;
-    int rank = 0;
-};
+#include "ks_dist.cuh"
 
 namespace ks {
 

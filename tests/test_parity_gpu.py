@@ -290,6 +290,26 @@ def test_reference_unit_tests_against_dropin():
     assert "21 | 21 passed" in r.stdout
 
 
+@pytest.mark.parametrize("shape", [(4, 8, 2048, 7), (2, 4, 4096, 200), (32, 8, 48, 48)])
+def test_peer_fused_combine_single_rank(shape):
+    """ks_dwconv1d_dw_f32_peer on a 1-rank communicator: stage 1 into the
+    IPC-exposed buffer, then the signal/wait/combine kernel; bits equal the
+    ordinary HIERARCHICAL dW, across calls (the epoch-parity double buffer)."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(7, B, H, L, K)
+    ref = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED)).copy()
+    comm = ks.Comm(ks.Comm.unique_id(), 1, 0)
+    peer = comm.peer(B, H, L, K)
+    try:
+        for _ in range(3):
+            got = host(peer.backward_weight(gy, x, K, FUSED))
+            assert same(got, ref)
+        assert not peer.timed_out()
+    finally:
+        peer.close()
+        comm.close()
+
+
 def test_nccl_combine_single_rank():
     """The C library's own NCCL communicator on this GPU (world size 1 -- the
     round's boxes have one GPU; N > 1 is covered by tests/test_dist_gloo.py):
