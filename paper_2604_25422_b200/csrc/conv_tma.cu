@@ -47,15 +47,41 @@ bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t 
     return r == CUDA_SUCCESS;
 }
 
-// kp[h, 0:Kp) = k[h, j] (forward) or k[h, K-1-j] (dX, the reference's
-// k[h, K-1-j] of src/conv_core.cpp:68), zero padded to Kp.
+// Padded view: the [rows, L] tensor as the 5-D tensor {4, 8, L/32, H, rows/H}
+// (floats, quads, 32-float pieces, channels, batch entries) with box
+// {4, 9, n, 1, depth}.  Quad 8 of every piece lies outside dim 1, so TMA
+// zero-fills it and each 32-float piece lands as a 36-float shared row: the
+// bank-conflict-free padded layout with no re-layout pass.  `depth` > 1 stacks
+// the same channel of consecutive batch entries (the dW kernel); the stencil
+// uses depth 1 with H = 1 (rows = channels x batch) or stacks channels via
+// dim 3 by passing chan_box > 1.
+bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
+                        int chan_box, int depth) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || L % 32 != 0 || H < 1 || rows % H != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+    if (n < 1 || n > 256 || chan_box < 1 || chan_box > 256 || depth < 1 || depth > 256) return false;
+    if (L / 32 >= (int64_t(1) << 31) || H >= (int64_t(1) << 31) || rows / H >= (int64_t(1) << 31)) return false;
+    const cuuint64_t dims[5] = {4, 8, static_cast<cuuint64_t>(L / 32), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(rows / H)};
+    const cuuint64_t strides[4] = {16, 128, static_cast<cuuint64_t>(L) * 4, static_cast<cuuint64_t>(L * H) * 4};
+    const cuuint32_t box[5] = {4, 9, static_cast<cuuint32_t>(n), static_cast<cuuint32_t>(chan_box),
+                               static_cast<cuuint32_t>(depth)};
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+// kp[h, 0:Kp) = `lead` zeros, then k[h, j] (forward) or k[h, K-1-j] (dX, the
+// reference's k[h, K-1-j] of src/conv_core.cpp:68), zero padded to Kp.
 __global__ void prep_taps(const float* __restrict__ k, float* __restrict__ kp, int64_t H, int64_t K, int64_t Kp,
-                          int reverse) {
+                          int reverse, int lead) {
     const int64_t n = H * Kp;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t h = i / Kp, j = i - h * Kp;
-        kp[i] = j < K ? k[h * K + (reverse ? K - 1 - j : j)] : 0.f;
+        const int64_t h = i / Kp, j = i - h * Kp - lead;
+        kp[i] = j >= 0 && j < K ? k[h * K + (reverse ? K - 1 - j : j)] : 0.f;
     }
 }
 

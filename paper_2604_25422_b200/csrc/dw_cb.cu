@@ -16,6 +16,7 @@
 // goes to part[g,h,j], and dw_sum_groups adds the G partials in ascending g.
 // No atomics: deterministic for a fixed shape.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
@@ -181,9 +182,19 @@ int dw_cb_groups(int64_t B, int64_t H, int64_t K) {
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(G, B)));
 }
 
+ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+                        int G, int mode, cudaStream_t st, bool* handled);
+
 ks_status dw_cb_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
                        int G, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
+    {  // padded TMA view (dw_pad.cu); KS_CB_IMPL=1 selects the kernels below (A/B knob)
+        const char* e = getenv("KS_CB_IMPL");
+        if (!(e && atoi(e) == 1)) {
+            const ks_status s = dw_pad_stage1(gy, x, part, B, H, L, K, G, mode, st, handled);
+            if (*handled) return s;
+        }
+    }
     if (!dw_cb_applies(B, H, L, K)) return KS_OK;
     int njg = 4;
     while (njg < 32 && njg * kJR < K) njg *= 2;

@@ -53,6 +53,12 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
                  : "memory");
 }
 
+// Plain arrive (release at CTA scope): consumer warps hand a stage back to
+// the producer lane of the padded-view kernels (stencil_pad.cu, dw_pad.cu).
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
         "{\n"
@@ -65,6 +71,25 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Wait with back-off: for a producer warp that would otherwise spin hot and
+// steal issue slots from the FMA warps it feeds.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+    uint32_t done;
+    for (;;) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "selp.u32 %0, 1, 0, p;\n"
+            "}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (done) return;
+        __nanosleep(128);
+    }
+}
+
 // 3-D tiled TMA load of one box into shared memory, completing on `bar`.
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
@@ -72,6 +97,16 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// 5-D tiled TMA load (the padded view of encode_padded_view).
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c2, int c3, int c4,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
         : "memory");
 }
 
@@ -121,5 +156,12 @@ __device__ __forceinline__ uint32_t swz(uint32_t i) {
 // violates TMA's constraints (the caller then uses the generic kernels).
 bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int inner, int box_rows,
                      int sw);
+
+// Host: the padded 5-D view {4, 8, L/32, H, rows/H} of a [rows, L] fp32 tensor
+// (rows = batch x H channels) with box {4, 9, n, chan_box, depth}: every
+// 32-float piece lands as a 36-float shared row whose last quad is zero
+// (conflict-free 128-bit reads 144 B apart, no re-layout pass).
+bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
+                        int chan_box, int depth);
 
 }  // namespace ks

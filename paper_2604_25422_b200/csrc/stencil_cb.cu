@@ -19,13 +19,14 @@
 //   * taps accumulate in ascending j from +0 (fmaf or mul+add), so results are
 //     bit-identical to the reference; tail taps past K are predicated off.
 #include <algorithm>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
 namespace ks {
 
-__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int);
+__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
 
 namespace {
 
@@ -47,6 +48,59 @@ struct CbGeom {
 };
 
 __device__ __forceinline__ int padi(int i) { return i + ((i >> 5) << 2); }
+
+// One thread's R = 32 outputs of a tile: acc[r] = sum_j pw[padi(pbase' + r + j)] * wk[j]
+// in ascending j from +0, over the padded window `pw` (thread's first tap at
+// padded index pbase) and the channel's taps `wk` (Kp floats, zero past K).
+template <bool FUSED>
+__device__ __forceinline__ void cb_tile(const float* pw, const float* wk, int pbase, int K, float (&acc)[kR]) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) acc[r] = 0.f;
+    // one 16-tap register window (compile-time sub-offsets), taps w16[0 .. 16),
+    // `nj` of them live; `base` = padded address of a 32-aligned logical index;
+    // the window starts `sub` (0 or 16, a literal) floats later
+    auto window = [&](const float* base, const int sub, const float* w16, int nj) {
+        float v[4 * kNV];
+#pragma unroll
+        for (int c = 0; c < kNV; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(base + sub + 4 * c + (((sub + 4 * c) >> 5) << 2));
+            v[4 * c + 0] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+        float w[kJS];
+#pragma unroll
+        for (int c = 0; c < kJS / 4; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(w16 + 4 * c);
+            w[4 * c + 0] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kJS; ++jj)
+            if (jj < nj) {
+#pragma unroll
+                for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[r + jj], w[jj]);
+            }
+    };
+    // 32 taps per iteration: windows at logical base + j0 and + j0 + 16.
+    // logical base + j0 is a multiple of 32, so its padded address is
+    // pbase + j0*36/32 and the +16 window starts 16 floats further.
+    const int Kfull = K & ~31;
+    for (int j0 = 0; j0 < Kfull; j0 += 32) {
+        const float* b0 = pw + pbase + (j0 >> 5) * 36;
+        window(b0, 0, wk + j0, kJS);
+        window(b0, 16, wk + j0 + 16, kJS);
+    }
+    if (Kfull < K) {
+        const float* b0 = pw + pbase + (Kfull >> 5) * 36;
+        const int rem = K - Kfull;
+        window(b0, 0, wk + Kfull, rem < kJS ? rem : kJS);
+        if (rem > kJS) window(b0, 16, wk + Kfull + 16, rem - kJS);
+    }
+}
 
 template <int NT, bool FUSED>
 __global__ void __launch_bounds__(NT)
@@ -100,53 +154,7 @@ stencil_cb(const __grid_constant__ CUtensorMap in_map, const float* __restrict__
         const int t0 = (tile - row * tiles_per_row) * g.T;
         if (t0 + tid * kR < L) {  // L % 32 == 0: a register tile is wholly in or out
             float acc[kR];
-#pragma unroll
-            for (int r = 0; r < kR; ++r) acc[r] = 0.f;
-            // one 16-tap register window at padded offset `po` (compile-time
-            // sub-offsets), taps wk[j0 .. j0+16), `nj` of them live
-            // `base` = padded address of a 32-aligned logical index; the window
-            // starts `sub` (0 or 16, a literal) floats later
-            auto window = [&](const float* base, const int sub, const float* w16, int nj) {
-                float v[4 * kNV];
-#pragma unroll
-                for (int c = 0; c < kNV; ++c) {
-                    const float4 q = *reinterpret_cast<const float4*>(base + sub + 4 * c + (((sub + 4 * c) >> 5) << 2));
-                    v[4 * c + 0] = q.x;
-                    v[4 * c + 1] = q.y;
-                    v[4 * c + 2] = q.z;
-                    v[4 * c + 3] = q.w;
-                }
-                float w[kJS];
-#pragma unroll
-                for (int c = 0; c < kJS / 4; ++c) {
-                    const float4 q = *reinterpret_cast<const float4*>(w16 + 4 * c);
-                    w[4 * c + 0] = q.x;
-                    w[4 * c + 1] = q.y;
-                    w[4 * c + 2] = q.z;
-                    w[4 * c + 3] = q.w;
-                }
-#pragma unroll
-                for (int jj = 0; jj < kJS; ++jj)
-                    if (jj < nj) {
-#pragma unroll
-                        for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[r + jj], w[jj]);
-                    }
-            };
-            // 32 taps per iteration: windows at logical base + j0 and + j0 + 16.
-            // logical base + j0 is a multiple of 32, so its padded address is
-            // pbase + j0*36/32 and the +16 window starts 16 floats further.
-            const int Kfull = K & ~31;
-            for (int j0 = 0; j0 < Kfull; j0 += 32) {
-                const float* b0 = pw + pbase + (j0 >> 5) * 36;
-                window(b0, 0, wk + j0, kJS);
-                window(b0, 16, wk + j0 + 16, kJS);
-            }
-            if (Kfull < K) {
-                const float* b0 = pw + pbase + (Kfull >> 5) * 36;
-                const int rem = K - Kfull;
-                window(b0, 0, wk + Kfull, rem < kJS ? rem : kJS);
-                if (rem > kJS) window(b0, 16, wk + Kfull + 16, rem - kJS);
-            }
+            cb_tile<FUSED>(pw, wk, pbase, K, acc);
             float* o = out + static_cast<int64_t>(row) * L + t0 + tid * kR;
 #pragma unroll
             for (int r = 0; r < kR; r += 4) st_cs_v4(o + r, make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]));
@@ -211,7 +219,7 @@ ks_status stencil_cb_f32(const float* in, const float* k, float* out, int64_t B,
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
     if (rc != KS_OK) return rc;
     prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
-        k, kp, H, K, g.Kp, reverse);
+        k, kp, H, K, g.Kp, reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;

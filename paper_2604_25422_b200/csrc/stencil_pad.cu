@@ -1,0 +1,265 @@
+// stencil_pad.cu -- compute-bound forward / dX (K > 32), sm_100a, fed straight
+// from TMA in the padded layout.
+//
+//   out[b,h,t] = sum_{j=0}^{K-1} in[b,h,t+j-off] * w[h,j]   (reference src/conv_core.cpp:21-75)
+//
+// The FMA inner loop wants each thread's 32-output register tile to read its
+// input window with 128-bit loads at compile-time offsets, bank-conflict free:
+// rows of 32 floats at a 36-float (144 B) pitch.  TMA writes that layout
+// itself: the tensor is viewed as {4 floats, 8 quads, L/32 pieces, H, B} and
+// loaded with box {4, 9, n, RPT, 1} -- quad 8 lies outside dim 1 and is
+// zero-filled, so every 32-float piece lands as a 36-float row.  No re-layout
+// pass, no producer warp: the CTA computes straight from the stage ring.
+//
+// The window must start on a 32-float piece: the taps are given `lead` =
+// (-off) mod 32 leading zeros (prep_taps), so the window origin t0 - off - lead
+// is a multiple of 32.  A leading zero tap adds x*0 = +-0 to an accumulator
+// that starts at +0, which leaves every partial sum unchanged (round to
+// nearest never yields -0 from a +0 start) -- the same argument that makes the
+// zero-filled halo exact -- so results stay bit-identical to the reference.
+//
+// Tiles: RPT consecutive channels of one batch entry x (TPR*32)-output pieces
+// of their rows; NT = 128 threads (one warp per SM sub-partition), thread
+// (r, lt) owns outputs [t0 + 32 lt, +32) of channel h0 + r.  NS-stage TMA ring
+// (one mbarrier per stage), one CTA barrier per tile before its stage is
+// refilled.
+#include <algorithm>
+#include <cstdlib>
+
+#include "ks_common.cuh"
+#include "ks_tma.cuh"
+
+namespace ks {
+
+__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
+
+namespace {
+
+constexpr int kR = 32;                       // outputs per thread
+constexpr int kJS = 16;                      // taps per register window
+constexpr int kNV = (kR + kJS - 1 + 3) / 4;  // float4 loads per window (12)
+
+struct PadGeom {
+    int RPT, TPR;      // channels per tile, threads per channel row (TPR*32 outputs)
+    int NR;            // padded 36-float rows per channel window (T/32 + Kp/32 [+1])
+    int NB, nbox;      // rows per TMA box, boxes per channel window (RPT == 1 when nbox > 1)
+    int Kp;            // taps (with lead zeros) padded to a multiple of 32
+    int Ke;            // taps incl. lead zeros (the live ones)
+    int base_row;      // (off + lead) / 32: window origin = t0/32 - base_row
+    int win_floats;    // RPT * nbox * NB * 36
+    int stage_bytes;   // window + RPT tap rows, 1024-aligned
+};
+
+// One thread's 32 outputs: acc[r] = sum_{j<Ke} win[S + r + j] * wk[j] in
+// ascending j from +0, where win is the thread's window starting at the padded
+// address pw + pbase (a 32-aligned logical index) and S = 0..3 the sub-quad
+// offset of its first tap.  Each 16-tap register window takes
+// ceil((S + 47) / 4) 128-bit loads (12 for S <= 1, 13 otherwise).
+template <int S, bool FUSED>
+__device__ __forceinline__ void tile32(const float* pw, const float* wk, int pbase, int Ke, float (&acc)[kR]) {
+    constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) acc[r] = 0.f;
+    auto window = [&](const float* base, const int sub, const float* w16, int nj) {
+        float v[4 * NV];
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(base + sub + 4 * c + (((sub + 4 * c) >> 5) << 2));
+            v[4 * c + 0] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+        float w[kJS];
+#pragma unroll
+        for (int c = 0; c < kJS / 4; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(w16 + 4 * c);
+            w[4 * c + 0] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+        }
+#pragma unroll
+        for (int jj = 0; jj < kJS; ++jj)
+            if (jj < nj) {
+#pragma unroll
+                for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[S + r + jj], w[jj]);
+            }
+    };
+    const int Kfull = Ke & ~31;
+    for (int j0 = 0; j0 < Kfull; j0 += 32) {
+        const float* b0 = pw + pbase + (j0 >> 5) * 36;
+        window(b0, 0, wk + j0, kJS);
+        window(b0, 16, wk + j0 + 16, kJS);
+    }
+    if (Kfull < Ke) {
+        const float* b0 = pw + pbase + (Kfull >> 5) * 36;
+        const int rem = Ke - Kfull;
+        window(b0, 0, wk + Kfull, rem < kJS ? rem : kJS);
+        if (rem > kJS) window(b0, 16, wk + Kfull + 16, rem - kJS);
+    }
+}
+
+template <int NT, int S, bool FUSED>
+__global__ void __launch_bounds__(NT + 32)
+stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out,
+            int H, int L, int tiles_per_row, int ntiles, PadGeom g, int NS) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = align_smem<1024>(smem_raw);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * g.stage_bytes);
+    uint64_t* empty = full + NS;
+    const int tid = threadIdx.x;
+    const int T = g.TPR * kR;
+
+    if (tid == 0) {
+        prefetch_tmap(&in_map);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NT / 32);
+        }
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (tid >= NT) {  // producer warp: one lane issues the loads, NS tiles ahead
+        if (tid != NT) return;
+        const int ngroups = H / g.RPT;  // channel groups per batch entry
+        const uint32_t tx_bytes = static_cast<uint32_t>(g.win_floats * 4 + g.RPT * g.Kp * 4);
+        int it = 0;
+        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+            const int stage = it % NS;
+            if (it >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((it / NS - 1) & 1));
+            const int rg = tile / tiles_per_row;
+            const int t0 = (tile - rg * tiles_per_row) * T;
+            const int b = rg / ngroups, h0 = (rg - b * ngroups) * g.RPT;
+            unsigned char* sb = smem + stage * g.stage_bytes;
+            mbar_arrive_expect_tx(&full[stage], tx_bytes);
+            const int r0 = t0 / 32 - g.base_row;
+            tma_load_5d(sb, &in_map, r0, h0, b, &full[stage]);
+            if (g.nbox > 1) tma_load_5d(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
+            bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kp,
+                      static_cast<uint32_t>(g.RPT * g.Kp) * 4u, &full[stage]);
+        }
+        return;
+    }
+
+    const int rsub = tid / g.TPR, lt = tid - rsub * g.TPR;
+    const int win_rows = g.nbox * g.NB;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+        const int stage = it % NS;
+        mbar_wait(&full[stage], static_cast<uint32_t>((it / NS) & 1));
+        const float* sw = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
+        const int rg = tile / tiles_per_row;
+        const int t0 = (tile - rg * tiles_per_row) * T;
+        const bool live = t0 + lt * kR < L;  // L % 32 == 0: a register tile is wholly in or out
+        float acc[kR];
+        if (live) tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, acc);
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+        if (live) {
+            float* o = out + static_cast<int64_t>(rg * g.RPT + rsub) * L + t0 + lt * kR;
+#pragma unroll
+            for (int r = 0; r < kR; r += 4) st_cs_v4(o + r, make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]));
+        }
+    }
+}
+
+int pad_smem(const PadGeom& g, int NS) { return NS * g.stage_bytes + 128 + 1024; }
+
+template <int NT, int S, bool FUSED>
+ks_status launch(const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H, int64_t L,
+                 const PadGeom& g, int NS, cudaStream_t st) {
+    auto kern = stencil_pad<NT, S, FUSED>;
+    const int smem = pad_smem(g, NS);
+    const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), NT + 32, smem);
+    const int T = g.TPR * kR;
+    const int tiles_per_row = static_cast<int>((L + T - 1) / T);
+    const int ntiles = static_cast<int>(B * H / g.RPT * tiles_per_row);
+    const int grid = std::min(ntiles, num_sms() * per_sm);
+    kern<<<grid, NT + 32, smem, st>>>(im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
+                                      g, NS);
+    return check_launch();
+}
+
+template <int NT>
+ks_status launch_s(int s, bool fused, const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H,
+                   int64_t L, const PadGeom& g, int NS, cudaStream_t st) {
+    switch (s) {
+        case 0: return fused ? launch<NT, 0, true>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<NT, 0, false>(im, kp, out, B, H, L, g, NS, st);
+        case 1: return fused ? launch<NT, 1, true>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<NT, 1, false>(im, kp, out, B, H, L, g, NS, st);
+        case 2: return fused ? launch<NT, 2, true>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<NT, 2, false>(im, kp, out, B, H, L, g, NS, st);
+        default: return fused ? launch<NT, 3, true>(im, kp, out, B, H, L, g, NS, st)
+                              : launch<NT, 3, false>(im, kp, out, B, H, L, g, NS, st);
+    }
+}
+
+int env_knob(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v && *v ? atoi(v) : dflt;
+}
+
+}  // namespace
+
+// Compute-bound fwd/dX from the padded TMA view (K > 32, L >= 2048,
+// L % 32 == 0).  *handled = false when the shape is outside the envelope.
+ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
+                          int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
+    *handled = false;
+    if (L % 32 != 0 || L < 2048 || L >= (int64_t(1) << 30) || K > 8192 || K <= 32) return KS_OK;
+    if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
+    const int NT = env_knob("KS_PAD_NT", 128) == 256 ? 256 : 128;  // tuning knob
+    PadGeom g{};
+    // window origin t0 - off - lead on a 32-float piece; the first tap sits
+    // `lead` floats in: `lead & ~3` leading zero taps plus a sub-quad offset S
+    const int lead = static_cast<int>((32 - off % 32) % 32);
+    const int S = lead & 3, zlead = lead - S;
+    g.Ke = static_cast<int>(K) + zlead;
+    g.Kp = (g.Ke + 31) / 32 * 32;
+    g.base_row = static_cast<int>((off + lead) / 32);
+    g.RPT = 1;
+    while (g.RPT < 8 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
+    g.TPR = NT / g.RPT;
+    const int T = g.TPR * kR;
+    g.NR = T / 32 + g.Kp / 32 + (S >= 2 ? 1 : 0);  // S >= 2: 13-quad windows read 4 floats further
+    if (g.NR <= 256) {
+        g.nbox = 1;
+        g.NB = g.NR;
+    } else if (g.RPT == 1 && g.NR <= 512) {
+        g.nbox = 2;  // second box 128-byte aligned: NB a multiple of 8 (8 rows = 1152 B)
+        g.NB = ((g.NR + 1) / 2 + 7) / 8 * 8;
+    } else {
+        return KS_OK;
+    }
+    g.win_floats = g.RPT * g.nbox * g.NB * 36;
+    g.stage_bytes = (g.win_floats * 4 + g.RPT * g.Kp * 4 + 1023) / 1024 * 1024;
+    if (B * H / g.RPT * ((L + T - 1) / T) >= (int64_t(1) << 31)) return KS_OK;
+    // stages: two in flight beyond the one being computed while the CTA count
+    // per SM stays >= 2; long K (>= 1024) computes ~100x longer than it loads
+    int NS = K >= 1024 ? 1 : 3;
+    while (NS > 1 && pad_smem(g, NS) > 110 * 1024) --NS;
+    if (env_knob("KS_PAD_NS", 0) > 0) NS = std::min(4, env_knob("KS_PAD_NS", 0));
+    if (pad_smem(g, NS) > 220 * 1024) return KS_OK;
+    CUtensorMap im;
+    if (!encode_padded_view(&im, in, B * H, L, H, g.NB, g.RPT, 1)) return KS_OK;
+
+    float* kp = nullptr;
+    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
+    if (rc != KS_OK) return rc;
+    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
+        k, kp, H, K, g.Kp, reverse, zlead);
+    rc = check_launch();
+    if (rc == KS_OK) {
+        const bool fused = mode == KS_MULADD_FUSED;
+        rc = NT == 256 ? launch_s<256>(S, fused, im, kp, out, B, H, L, g, NS, st)
+                       : launch_s<128>(S, fused, im, kp, out, B, H, L, g, NS, st);
+    }
+    scratch_free(kp, st);
+    *handled = true;
+    return rc;
+}
+
+}  // namespace ks

@@ -28,9 +28,11 @@
 
 namespace ks {
 
-__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int);
+__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
 ks_status stencil_cb_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
                          int64_t off, int reverse, int mode, cudaStream_t st, bool* handled);
+ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
+                          int64_t off, int reverse, int mode, cudaStream_t st, bool* handled);
 
 namespace {
 
@@ -248,8 +250,11 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     *handled = false;
     if (L % kIn != 0 || L >= (int64_t(1) << 30) || K > 8192) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
-    if (env_int("KS_STENCIL_CB", 1)) {  // compute-bound long-K kernel (stencil_cb.cu)
-        const ks_status s = stencil_cb_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
+    if (env_int("KS_STENCIL_CB", 1)) {  // compute-bound long-K kernels
+        // padded TMA view (stencil_pad.cu); KS_CB_IMPL=1 selects stencil_cb.cu (A/B knob)
+        const ks_status s = env_int("KS_CB_IMPL", 0) == 1
+                                ? stencil_cb_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled)
+                                : stencil_pad_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }
     int R, NT;
@@ -305,7 +310,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
     if (rc != KS_OK) return rc;
     prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
-        k, kp, H, K, g.Kp, reverse);
+        k, kp, H, K, g.Kp, reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;

@@ -17,7 +17,7 @@ model) extends to B200:
   (TMA boxes overlap by 32*HH floats per side per tile);
 * ``plan(path, B, H, L, K)`` -- which kernel family runs, its tile and grid
   (mirrors the host dispatch in csrc/: conv_fwd.cu, stencil_tma.cu,
-  stencil_cb.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
+  stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
 
 ``tests/test_traffic.py`` checks memory_traffic against the ncu DRAM bytes
 committed in profiles/ncu_summary.json.
@@ -41,8 +41,7 @@ def _stencil_tier(L: int, K: int):
     if L % 32 != 0 or K > 8192:
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
     if K > 32 and L >= 2048:
-        nt = 256 if L >= 8192 else 128 if L >= 4096 else 64
-        return "stencil_cb", 32, nt
+        return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
     if L >= 1024:
         nt = 256 if L >= 4096 else 128 if L >= 2048 else 64
         return "stencil_tma", 16, nt
@@ -56,7 +55,7 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
             njg *= 2
         njt = math.ceil(K / (njg * 32))
         G = max(1, min(math.ceil(2048 / (H * njt)), B))
-        return "dw_cb", G
+        return "dw_pad", G
     groups8 = math.ceil(K / 8)
     nj = 1
     while nj < 8 and nj < groups8:
@@ -87,7 +86,7 @@ def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hie
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
         kp = 4 * H * (math.ceil(K / 32) * 32)  # prep_taps writes kp, the kernel reads it back
-        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_cb") else 0)
+        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad") else 0)
     if p["kernel"] == "dw_pairwise_tma":
         return base
     return base + 2 * p["partials_bytes"]  # partials written by stage 1, read by stage 2

@@ -52,7 +52,7 @@ SHAPES = [(1, 1, 3, 3), (2, 3, 17, 5), (2, 2, 5, 4), (3, 2, 33, 8), (2, 2, 10, 1
           (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256),
           # short rows (rows_short.cu), incl. the paper's (L,K) = (48,48) and K > L
           (16, 8, 48, 48), (5, 3, 100, 9), (2, 3, 512, 64), (3, 2, 1020, 5), (7, 5, 96, 97), (70, 3, 48, 48),
-          # compute-bound dW (dw_cb.cu): K >= 128, ragged tap tiles
+          # compute-bound dW (dw_pad.cu): K >= 128, ragged tap tiles, odd p (shifted tap origin)
           (2, 3, 2048, 130), (1, 2, 4096, 200), (3, 1, 6144, 555)]
 
 
@@ -253,6 +253,30 @@ def test_full_config_channel_slices(oracle, cfg):
             assert same(dkp[h:h + 1], oracle.backward_weight(gs, xs, K, PAIRWISE))
     del x, gy, y, dx
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape", [(24, 256, 2048, 128), (6, 128, 16384, 64), (40, 64, 2048, 300),
+                                   (8, 32, 4096, 77), (4, 16, 2048, 1000), (4, 8, 2048, 58)])
+def test_padded_view_kernels_many_tiles(oracle, shape):
+    """Compute-bound kernels fed by the padded TMA view (stencil_pad, dw_pad)
+    with several tiles / work items per CTA, so every stage and both mbarrier
+    phases recur (and RPT = 2 channels per tile at L = 2048): sampled channels
+    bitwise (y, dX) in both modes, dW to tolerance and run-to-run deterministic."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(3, B, H, L, K)
+    kh = k.cpu().numpy()
+    for m in (SEPARATE, FUSED):
+        y = ks.forward(x, k, m)
+        dx = ks.backward_input(gy, k, m)
+        dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
+        assert same(dk, host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m)))
+        for h in (0, H // 3, H - 1):
+            xs, gs = _channel_slice(x, h), _channel_slice(gy, h)
+            ks_ = np.ascontiguousarray(kh[h:h + 1])
+            assert same(_channel_slice(y, h), oracle.forward(xs, ks_, m)), (h, m)
+            assert same(_channel_slice(dx, h), oracle.backward_input(gs, ks_, m)), (h, m)
+            truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+            assert normwise(dk[h:h + 1], truth) <= HIER_TOL
 
 
 def test_full_config3_identities():

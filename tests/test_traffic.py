@@ -15,9 +15,9 @@ def test_logical_traffic_matches_reference_formula():
 
 def test_plan_dispatch_tiers():
     assert traffic.plan("fwd", 256, 512, 8192, 7)["kernel"] == "stencil_tma"
-    assert traffic.plan("fwd", 64, 128, 4096, 4096)["kernel"] == "stencil_cb"
+    assert traffic.plan("fwd", 64, 128, 4096, 4096)["kernel"] == "stencil_pad"
     assert traffic.plan("fwd", 16384, 128, 48, 48)["kernel"] == "stencil_rows"
-    assert traffic.plan("dw", 64, 128, 4096, 4096)["kernel"] == "dw_cb"
+    assert traffic.plan("dw", 64, 128, 4096, 4096)["kernel"] == "dw_pad"
     assert traffic.plan("dw", 256, 512, 8192, 7)["kernel"] == "dw_tma"
     assert traffic.plan("dw", 256, 512, 8192, 7, "pairwise")["kernel"] == "dw_pairwise_tma"
 
