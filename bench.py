@@ -92,6 +92,46 @@ def ncu_traffic(config_name):
         return None
 
 
+def pcie_probe(dev, nbytes=1 << 30, reps=3):
+    """Pinned host <-> device copy rates (GB/s): H2D alone, D2H alone, and both
+    directions at once on two streams -- the roof of the e2e number."""
+    import torch
+
+    n = nbytes // 4
+    hs = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    hd = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    da = torch.empty(n, dtype=torch.float32, device=dev)
+    db = torch.empty(n, dtype=torch.float32, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def timed(fn):
+        best = float("inf")
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t0 = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            best = min(best, time.perf_counter() - t0)
+        return best
+
+    def h2d():
+        with torch.cuda.stream(s1):
+            da.copy_(hs, non_blocking=True)
+
+    def d2h():
+        with torch.cuda.stream(s2):
+            hd.copy_(db, non_blocking=True)
+
+    def both():
+        h2d()
+        d2h()
+
+    t_h, t_d, t_b = timed(h2d), timed(d2h), timed(both)
+    del hs, hd, da, db
+    return {"h2d_gbs": round(nbytes / t_h / 1e9, 1), "d2h_gbs": round(nbytes / t_d / 1e9, 1),
+            "bidir_gbs": round(2 * nbytes / t_b / 1e9, 1)}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
@@ -419,6 +459,14 @@ def run_ours(args, cfg_name, cfg):
         e2e = {"value": round(world * 3 * pb / t_host / 1e9, 2), "unit": "GB/s",
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps, "path": path}
+        # the e2e roof: the step's PCIe bytes at the link's measured rates
+        # (H2D and D2H overlap on separate copy engines)
+        pcie = pcie_probe(dev)
+        bound_s = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
+                      (h2d + d2h) / (pcie["bidir_gbs"] * 1e9))
+        pcie["bound_ms"] = round(bound_s * 1e3, 2)
+        pcie["frac"] = round(bound_s / t_host, 4)
+        e2e["pcie"] = pcie
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

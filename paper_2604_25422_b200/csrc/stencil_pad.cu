@@ -35,6 +35,7 @@ __global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, 
 
 namespace {
 
+constexpr int kNT = 128;                     // FMA threads per CTA (one warp per SM sub-partition)
 constexpr int kR = 32;                       // outputs per thread
 constexpr int kJS = 16;                      // taps per register window
 constexpr int kNV = (kR + kJS - 1 + 3) / 4;  // float4 loads per window (12)
@@ -100,8 +101,12 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     }
 }
 
-template <int NT, int S, bool FUSED>
-__global__ void __launch_bounds__(NT + 32)
+// PROD: one extra warp whose lane 0 keeps the ring NS tiles ahead and consumer
+// warps release a stage each as soon as they are done with it (moderate K,
+// where tiles are short); !PROD: thread 0 refills a stage after a CTA barrier
+// (long K, K >= 1024, where one stage suffices and the barrier is rare).
+template <int S, bool FUSED, bool PROD>
+__global__ void __launch_bounds__(kNT + (PROD ? 32 : 0))
 stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out,
             int H, int L, int tiles_per_row, int ntiles, PadGeom g, int NS) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -110,37 +115,48 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     uint64_t* empty = full + NS;
     const int tid = threadIdx.x;
     const int T = g.TPR * kR;
+    const int ngroups = H / g.RPT;  // channel groups per batch entry
+    const uint32_t tx_bytes = static_cast<uint32_t>(g.win_floats * 4 + g.RPT * g.Kp * 4);
+    auto issue = [&](int stage, int tile) {
+        const int rg = tile / tiles_per_row;
+        const int t0 = (tile - rg * tiles_per_row) * T;
+        const int b = rg / ngroups, h0 = (rg - b * ngroups) * g.RPT;
+        unsigned char* sb = smem + stage * g.stage_bytes;
+        mbar_arrive_expect_tx(&full[stage], tx_bytes);
+        const int r0 = t0 / 32 - g.base_row;
+        tma_load_5d(sb, &in_map, r0, h0, b, &full[stage]);
+        if (g.nbox > 1) tma_load_5d(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
+        bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kp,
+                  static_cast<uint32_t>(g.RPT * g.Kp) * 4u, &full[stage]);
+    };
 
     if (tid == 0) {
         prefetch_tmap(&in_map);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NT / 32);
+            mbar_init(&empty[s], kNT / 32);
         }
         fence_mbar_init();
     }
     __syncthreads();
 
-    if (tid >= NT) {  // producer warp: one lane issues the loads, NS tiles ahead
-        if (tid != NT) return;
-        const int ngroups = H / g.RPT;  // channel groups per batch entry
-        const uint32_t tx_bytes = static_cast<uint32_t>(g.win_floats * 4 + g.RPT * g.Kp * 4);
-        int it = 0;
-        for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
-            const int stage = it % NS;
-            if (it >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((it / NS - 1) & 1));
-            const int rg = tile / tiles_per_row;
-            const int t0 = (tile - rg * tiles_per_row) * T;
-            const int b = rg / ngroups, h0 = (rg - b * ngroups) * g.RPT;
-            unsigned char* sb = smem + stage * g.stage_bytes;
-            mbar_arrive_expect_tx(&full[stage], tx_bytes);
-            const int r0 = t0 / 32 - g.base_row;
-            tma_load_5d(sb, &in_map, r0, h0, b, &full[stage]);
-            if (g.nbox > 1) tma_load_5d(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
-            bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kp,
-                      static_cast<uint32_t>(g.RPT * g.Kp) * 4u, &full[stage]);
+    if constexpr (PROD) {
+        if (tid >= kNT) {  // producer warp: lane 0 issues the loads, NS tiles ahead
+            if (tid != kNT) return;
+            int it = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
+                const int stage = it % NS;
+                if (it >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((it / NS - 1) & 1));
+                issue(stage, tile);
+            }
+            return;
         }
-        return;
+    } else {
+        if (tid == 0)
+            for (int s = 0; s < NS; ++s) {
+                const int t = blockIdx.x + s * gridDim.x;
+                if (t < ntiles) issue(s, t);
+            }
     }
 
     const int rsub = tid / g.TPR, lt = tid - rsub * g.TPR;
@@ -155,8 +171,16 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         const bool live = t0 + lt * kR < L;  // L % 32 == 0: a register tile is wholly in or out
         float acc[kR];
         if (live) tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, acc);
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+        if constexpr (PROD) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+        } else {
+            __syncthreads();  // stage consumed by every thread
+            if (tid == 0) {
+                const int nt = tile + NS * gridDim.x;
+                if (nt < ntiles) issue(stage, nt);
+            }
+        }
         if (live) {
             float* o = out + static_cast<int64_t>(rg * g.RPT + rsub) * L + t0 + lt * kR;
 #pragma unroll
@@ -167,33 +191,34 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
 
 int pad_smem(const PadGeom& g, int NS) { return NS * g.stage_bytes + 128 + 1024; }
 
-template <int NT, int S, bool FUSED>
+template <int S, bool FUSED, bool PROD>
 ks_status launch(const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H, int64_t L,
                  const PadGeom& g, int NS, cudaStream_t st) {
-    auto kern = stencil_pad<NT, S, FUSED>;
+    auto kern = stencil_pad<S, FUSED, PROD>;
+    constexpr int threads = kNT + (PROD ? 32 : 0);
     const int smem = pad_smem(g, NS);
-    const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), NT + 32, smem);
+    const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);
     const int T = g.TPR * kR;
     const int tiles_per_row = static_cast<int>((L + T - 1) / T);
     const int ntiles = static_cast<int>(B * H / g.RPT * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
-    kern<<<grid, NT + 32, smem, st>>>(im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
+    kern<<<grid, threads, smem, st>>>(im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
                                       g, NS);
     return check_launch();
 }
 
-template <int NT>
+template <bool PROD>
 ks_status launch_s(int s, bool fused, const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H,
                    int64_t L, const PadGeom& g, int NS, cudaStream_t st) {
     switch (s) {
-        case 0: return fused ? launch<NT, 0, true>(im, kp, out, B, H, L, g, NS, st)
-                             : launch<NT, 0, false>(im, kp, out, B, H, L, g, NS, st);
-        case 1: return fused ? launch<NT, 1, true>(im, kp, out, B, H, L, g, NS, st)
-                             : launch<NT, 1, false>(im, kp, out, B, H, L, g, NS, st);
-        case 2: return fused ? launch<NT, 2, true>(im, kp, out, B, H, L, g, NS, st)
-                             : launch<NT, 2, false>(im, kp, out, B, H, L, g, NS, st);
-        default: return fused ? launch<NT, 3, true>(im, kp, out, B, H, L, g, NS, st)
-                              : launch<NT, 3, false>(im, kp, out, B, H, L, g, NS, st);
+        case 0: return fused ? launch<0, true, PROD>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<0, false, PROD>(im, kp, out, B, H, L, g, NS, st);
+        case 1: return fused ? launch<1, true, PROD>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<1, false, PROD>(im, kp, out, B, H, L, g, NS, st);
+        case 2: return fused ? launch<2, true, PROD>(im, kp, out, B, H, L, g, NS, st)
+                             : launch<2, false, PROD>(im, kp, out, B, H, L, g, NS, st);
+        default: return fused ? launch<3, true, PROD>(im, kp, out, B, H, L, g, NS, st)
+                              : launch<3, false, PROD>(im, kp, out, B, H, L, g, NS, st);
     }
 }
 
@@ -211,7 +236,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     *handled = false;
     if (L % 32 != 0 || L < 2048 || L >= (int64_t(1) << 30) || K > 8192 || K <= 32) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
-    const int NT = env_knob("KS_PAD_NT", 128) == 256 ? 256 : 128;  // tuning knob
+    constexpr int NT = kNT;
     PadGeom g{};
     // window origin t0 - off - lead on a 32-float piece; the first tap sits
     // `lead` floats in: `lead & ~3` leading zero taps plus a sub-quad offset S
@@ -254,8 +279,10 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;
-        rc = NT == 256 ? launch_s<256>(S, fused, im, kp, out, B, H, L, g, NS, st)
-                       : launch_s<128>(S, fused, im, kp, out, B, H, L, g, NS, st);
+        // long K: one stage, refilled after a CTA barrier; moderate K: producer lane
+        const bool prod = env_knob("KS_PAD_PROD", K >= 1024 ? 0 : 1) != 0;
+        rc = prod ? launch_s<true>(S, fused, im, kp, out, B, H, L, g, NS, st)
+                  : launch_s<false>(S, fused, im, kp, out, B, H, L, g, NS, st);
     }
     scratch_free(kp, st);
     *handled = true;
