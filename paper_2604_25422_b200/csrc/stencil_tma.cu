@@ -259,6 +259,10 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     }
     int R, NT;
     pick_tile(L, K, &R, &NT);
+    if (env_int("KS_STENCIL_R", 0) == 32 && L >= 2048) {  // tuning knob: R = 32 register tiles at short K
+        R = 32;
+        NT = L >= 8192 ? 256 : L >= 4096 ? 128 : 64;
+    }
     if (R == 16 && env_int("KS_STENCIL_NT", 0) > 0) {  // tuning knob (bench sweeps)
         const int nt = env_int("KS_STENCIL_NT", 0);
         if ((nt == 64 || nt == 128 || nt == 256) && nt * R <= L) NT = nt;
@@ -297,13 +301,13 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     // sweep of NT in {128,256} x NS in {2,3,4,6,8} spans 5.9-6.3 TB/s)
     int NS = 3;
     while (NS > 2 && stencil_smem_bytes(g, NS, tma_out) > 110 * 1024) --NS;
-    if (env_int("KS_STENCIL_NS", 0) > 0) NS = std::min(8, env_int("KS_STENCIL_NS", 0));  // tuning knob
     if (R == 32) {
         // compute-bound: spend shared memory on resident warps rather than deep
         // prefetch.  With K >= 1024 a tile's FMAs (R*K per thread) outlast its
         // load by ~100x and one stage suffices; shorter K keeps one tile in flight.
         NS = K >= 1024 ? 1 : 2;
     }
+    if (env_int("KS_STENCIL_NS", 0) > 0) NS = std::min(8, env_int("KS_STENCIL_NS", 0));  // tuning knob
     if (stencil_smem_bytes(g, NS, tma_out) > 220 * 1024) return KS_OK;
 
     float* kp = nullptr;
