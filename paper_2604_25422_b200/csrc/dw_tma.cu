@@ -15,10 +15,11 @@
 // part[g,h,j]; dw_sum_groups (conv_dw.cu) adds the G partials in ascending g.
 // No atomics anywhere: the result is a deterministic function of the shape.
 //
-// (JR, TB) = (8, 8) for K <= 8 (memory-bound, e.g. BASELINE config 3) and
-// (16, 16) for longer K, where 256 FMAs per 13 shared loads keep the FMA pipe
+// (JR, TB) = (8, 8) for K <= 8 (memory-bound, e.g. BASELINE config 3),
+// (16, 8) for 8 < K <= 16 (config 5a) and (16, 16) for longer K, where 256 FMAs per 13 shared loads keep the FMA pipe
 // fed (compute-bound, configs 2 / 4 / 5b / 5c).
 #include <algorithm>
+#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
@@ -47,8 +48,8 @@ __device__ __forceinline__ int block_t(int q) {
     else return ((q & 31) * 2 + ((q >> 5) & 1) + (q >> 6) * 64) * TB;
 }
 
-template <int JR, int TB, int NJ, int S, bool FUSED>
-__global__ void __launch_bounds__(kThreads)
+template <int JR, int TB, int NJ, int S, bool FUSED, bool PROD>
+__global__ void __launch_bounds__(kThreads + (PROD ? 32 : 0))
 dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUtensorMap x_map,
        const __grid_constant__ CUtensorMap x_tail_map, float* __restrict__ part, int B, int H, int L, int K, int p,
        int G, int NJT, DwGeomT g, int NS) {
@@ -80,11 +81,15 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int xr_rel = (xoff - D) / kDwIn;  // exact division
     const int A = D & ~3;                   // D & 3 == S
 
+    uint64_t* empty = full + NS;
     if (tid == 0) {
         prefetch_tmap(&gy_map);
         prefetch_tmap(&x_map);
         prefetch_tmap(&x_tail_map);
-        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kThreads / 32);
+        }
         fence_mbar_init();
     }
     __syncthreads();
@@ -101,8 +106,22 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         tma_load_3d(sb + g.gy_bytes, &x_map, 0, xr, row, &full[stage]);
         tma_load_3d(sb + g.gy_bytes + kDwMain * kDwIn * 4, &x_tail_map, 0, xr + kDwMain, row, &full[stage]);
     };
-    if (tid == 0)
-        for (int s = 0; s < NS && s < nunits; ++s) issue(s, s);
+    if constexpr (PROD) {
+        // producer warp: lane 0 keeps the ring NS items ahead; consumer warps
+        // release a stage each as soon as they are done (no CTA barrier)
+        if (tid >= kThreads) {
+            if (tid == kThreads)
+                for (int u = 0; u < nunits; ++u) {
+                    const int stage = u % NS;
+                    if (u >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((u / NS - 1) & 1));
+                    issue(stage, u);
+                }
+            return;
+        }
+    } else {
+        if (tid == 0)
+            for (int s = 0; s < NS && s < nunits; ++s) issue(s, s);
+    }
 
     float acc[JR];
 #pragma unroll
@@ -143,8 +162,13 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                     for (int jj = 0; jj < JR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
             }
         }
-        __syncthreads();
-        if (tid == 0 && u + NS < nunits) issue(stage, u + NS);
+        if constexpr (PROD) {
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
+        } else {
+            __syncthreads();
+            if (tid == 0 && u + NS < nunits) issue(stage, u + NS);
+        }
     }
 
 #pragma unroll
@@ -159,7 +183,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 #pragma unroll
         for (int jj = 0; jj < JR; ++jj) red[warp][jj] = acc[jj];
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");  // the consumer warps
     constexpr int WPG = NTS / 32;  // warps per tap group
     if (tid < JT) {
         const int gj = tid / JR, jj = tid % JR;
@@ -171,17 +195,18 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     }
 }
 
-template <int JR, int TB, int NJ, bool FUSED>
+template <int JR, int TB, int NJ, bool FUSED, bool PROD>
 ks_status launch(int s, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt, float* part, int64_t B,
                  int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
-    const int smem = NS * g.stage_bytes + 64 + 1024;
+    const int smem = NS * g.stage_bytes + 128 + 1024;
+    constexpr int threads = kThreads + (PROD ? 32 : 0);
     const unsigned blocks = static_cast<unsigned>(int64_t(G) * H * NJT);
     const int p = static_cast<int>(K / 2);
 #define KS_DW_CASE(SV)                                                                                        \
     case SV: {                                                                                                \
-        auto kern = dw_tma<JR, TB, NJ, SV, FUSED>;                                                            \
-        prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                \
-        kern<<<blocks, kThreads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),      \
+        auto kern = dw_tma<JR, TB, NJ, SV, FUSED, PROD>;                                                      \
+        prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);                                 \
+        kern<<<blocks, threads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),       \
                                              static_cast<int>(L), static_cast<int>(K), p, G, NJT, g, NS);     \
         break;                                                                                                \
     }
@@ -200,8 +225,12 @@ template <int JR, int TB, int NJ>
 ks_status launch_m(int s, bool fused, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt,
                    float* part, int64_t B, int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS,
                    cudaStream_t st) {
-    return fused ? launch<JR, TB, NJ, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
-                 : launch<JR, TB, NJ, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
+    const char* e = getenv("KS_DWTMA_PROD");  // A/B knob: 1 = producer lane, no CTA barrier per item
+    if (e && atoi(e) == 1)
+        return fused ? launch<JR, TB, NJ, true, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
+                     : launch<JR, TB, NJ, false, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
+    return fused ? launch<JR, TB, NJ, true, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
+                 : launch<JR, TB, NJ, false, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
 }
 
 }  // namespace
@@ -216,8 +245,12 @@ ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B,
         return KS_OK;
     // (8,8) with 1-2 tap groups up to K = 16; (16,16) with >= 2 tap groups beyond
     // (a t-slice must cover a whole 16-wide block of the 2048-wide work item)
-    const int JR = K <= 16 ? 8 : 16;
-    int nj = JR == 8 ? 1 : 2;
+    // 8 < K <= 16: one tap group of 16 taps over 8-wide t blocks (16 x 8 FMAs
+    // per 2 gy + 6-7 x loads, half the shared traffic of two 8-tap groups)
+    const char* e16 = getenv("KS_DWTMA_J16");  // A/B knob: 0 = two 8-tap groups
+    const bool j16 = K > 8 && K <= 16 && !(e16 && *e16 == '0');
+    const int JR = K <= 16 && !j16 ? 8 : 16;
+    int nj = JR == 8 || j16 ? 1 : 2;
     while (nj < 8 && nj * JR < K) nj *= 2;
     const int njt = static_cast<int>((K + nj * JR - 1) / (nj * JR));
     if (int64_t(G) * H * njt >= (int64_t(1) << 31)) return KS_OK;
@@ -235,6 +268,7 @@ ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B,
     const int s = (4 - p % 4) % 4;
     const bool fused = mode == KS_MULADD_FUSED;
     *handled = true;
+    if (j16) return launch_m<16, 8, 1>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
     if (JR == 8)
         return nj == 1 ? launch_m<8, 8, 1>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st)
                        : launch_m<8, 8, 2>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);

@@ -49,7 +49,7 @@ SHAPES = [(1, 1, 3, 3), (2, 3, 17, 5), (2, 2, 5, 4), (3, 2, 33, 8), (2, 2, 10, 1
           (1, 1, 5000, 33), (2, 1, 8192, 7), (1, 2, 1001, 2), (2, 2, 6, 40), (1, 1, 4096, 4096),
           # one shape per TMA kernel variant (register tile R x threads NT, dW tap blocking)
           (2, 2, 2048, 33), (1, 2, 4096, 100), (1, 1, 8192, 48), (2, 2, 1024, 48), (2, 1, 2048, 12),
-          (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256),
+          (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256), (4, 4, 4096, 16), (3, 2, 2048, 11),
           # short rows (rows_short.cu), incl. the paper's (L,K) = (48,48) and K > L
           (16, 8, 48, 48), (5, 3, 100, 9), (2, 3, 512, 64), (3, 2, 1020, 5), (7, 5, 96, 97), (70, 3, 48, 48),
           # compute-bound dW (dw_pad.cu): K >= 128, ragged tap tiles, odd p (shifted tap origin)
