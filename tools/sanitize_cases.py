@@ -36,4 +36,24 @@ for (B, H, L, K) in shapes:
             if s != ks.HIERARCHICAL:
                 assert np.array_equal(dk.cpu().numpy(), o.backward_weight(gy, x, K, s, c, mode))
     yh, dxh, dkh = ks.step_host(x, k, gy, scheme=ks.HIERARCHICAL, mode=1)
+
+# the padded-TMA-view kernels (stencil_pad, dw_pad) with several tiles / work
+# items per CTA, so every stage ring slot and both mbarrier phases recur:
+# (32,64,2048,64) -> 1024 fwd/dX tiles over <= 444 CTAs; (32,256,2048,128) ->
+# 4 dW work items per CTA (> NS = 3 stages); odd p (K = 150) shifts the tap origin
+for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150)]:
+    x, k, gy = o.fill_inputs(5, B, H, L, K)
+    dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
+    y = ks.forward(dx_, dk_, 1)
+    d = ks.backward_input(dgy, dk_, 1)
+    dk = ks.backward_weight(dgy, dx_, K, ks.HIERARCHICAL, 0, 1)
+    torch.cuda.synchronize()
+    xs = np.ascontiguousarray(x[:, :1])
+    gs = np.ascontiguousarray(gy[:, :1])
+    kk = np.ascontiguousarray(k[:1])
+    assert np.array_equal(y.cpu().numpy()[:, :1], o.forward(xs, kk, 1))
+    assert np.array_equal(d.cpu().numpy()[:, :1], o.backward_input(gs, kk, 1))
+    truth = o.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+    err = np.abs(dk.cpu().numpy()[:1] - truth).max() / np.abs(truth).max()
+    assert err <= 1e-4, err
 print("sanitize cases ok")
