@@ -11,8 +11,9 @@
 // window as 36-float padded rows (box {4, 9, n, 1, 1} of the 5-D view, quad 8
 // zero-filled), so the CTA computes straight from an NS-stage ring with no
 // re-layout; one producer lane keeps the ring NS items ahead (full / empty
-// mbarriers, consumer warps release a stage as soon as they are done with it).  The x window must start on a 32-float piece, so tap tiles start
-// at j0 = base + jt*JT with base = (p mod 32) - 32 (or 0), making t0 + j0 - p
+// mbarriers; every consumer thread arrives on a stage's empty barrier once it
+// is done with it).  The x window must start on a 32-float piece, so tap
+// tiles start at j0 = base + jt*JT with base = (p mod 32) - 32 (or 0), making t0 + j0 - p
 // a multiple of 32; taps outside [0, K) are computed on zero-weight and not
 // written.  Accumulators stay in registers across all the CTA's work items;
 // then the NTS partials of each tap are added in fixed t-slice order, one
@@ -73,7 +74,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         prefetch_tmap(&x_map);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kNT / 32);
+            mbar_init(&empty[s], kNT);
         }
         fence_mbar_init();
     }
@@ -138,8 +139,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
             window(0);
             window(16);
         }
-        __syncwarp();
-        if ((tid & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+        mbar_arrive(&empty[stage]);  // this thread is done with the stage
     }
 
     // fixed-order reduction over the NTS t-slices of each tap group; the stage

@@ -88,7 +88,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         prefetch_tmap(&x_tail_map);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kThreads / 32);
+            mbar_init(&empty[s], kThreads);
         }
         fence_mbar_init();
     }
@@ -107,8 +107,8 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         tma_load_3d(sb + g.gy_bytes + kDwMain * kDwIn * 4, &x_tail_map, 0, xr + kDwMain, row, &full[stage]);
     };
     if constexpr (PROD) {
-        // producer warp: lane 0 keeps the ring NS items ahead; consumer warps
-        // release a stage each as soon as they are done (no CTA barrier)
+        // producer warp: lane 0 keeps the ring NS items ahead; consumer
+        // threads release a stage as soon as they are done (no CTA barrier)
         if (tid >= kThreads) {
             if (tid == kThreads)
                 for (int u = 0; u < nunits; ++u) {
@@ -163,8 +163,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
             }
         }
         if constexpr (PROD) {
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[stage]);
+            mbar_arrive(&empty[stage]);  // this thread is done with the stage
         } else {
             __syncthreads();
             if (tid == 0 && u + NS < nunits) issue(stage, u + NS);

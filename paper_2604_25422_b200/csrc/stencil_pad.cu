@@ -101,8 +101,8 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     }
 }
 
-// PROD: one extra warp whose lane 0 keeps the ring NS tiles ahead and consumer
-// warps release a stage each as soon as they are done with it (moderate K,
+// PROD: one extra warp whose lane 0 keeps the ring NS tiles ahead, and every
+// consumer thread releases a stage as soon as it is done with it (moderate K,
 // where tiles are short); !PROD: thread 0 refills a stage after a CTA barrier
 // (long K, K >= 1024, where one stage suffices and the barrier is rare).
 template <int S, bool FUSED, bool PROD>
@@ -134,7 +134,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         prefetch_tmap(&in_map);
         for (int s = 0; s < NS; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kNT / 32);
+            mbar_init(&empty[s], kNT);
         }
         fence_mbar_init();
     }
@@ -172,8 +172,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         float acc[kR];
         if (live) tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, acc);
         if constexpr (PROD) {
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(&empty[stage]);  // this warp is done with the stage
+            mbar_arrive(&empty[stage]);  // this thread is done with the stage
         } else {
             __syncthreads();  // stage consumed by every thread
             if (tid == 0) {
@@ -229,12 +228,12 @@ int env_knob(const char* name, int dflt) {
 
 }  // namespace
 
-// Compute-bound fwd/dX from the padded TMA view (K > 32, L >= 2048,
+// Compute-bound fwd/dX from the padded TMA view (K > 32, L >= 1024,
 // L % 32 == 0).  *handled = false when the shape is outside the envelope.
 ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
                           int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
-    if (L % 32 != 0 || L < 2048 || L >= (int64_t(1) << 30) || K > 8192 || K <= 32) return KS_OK;
+    if (L % 32 != 0 || L < 1024 || L >= (int64_t(1) << 30) || K > 8192 || K <= 32) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
     constexpr int NT = kNT;
     PadGeom g{};

@@ -40,7 +40,7 @@ def _stencil_tier(L: int, K: int):
         return "stencil_rows", 16, None
     if L % 32 != 0 or K > 8192:
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
-    if K > 32 and L >= 2048:
+    if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
     if L >= 1024:
         nt = 256 if L >= 4096 else 128 if L >= 2048 else 64
