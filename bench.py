@@ -377,6 +377,55 @@ def run_ours(args, cfg_name, cfg):
         step(evs[i])
     end.record(stream)
     torch.cuda.synchronize()
+
+    # The step proper: forward, then the layer's backward in ONE call
+    # (ks_dwconv1d_bwd_f32: dX and dW from a single pass over gy and x where
+    # the fused kernel applies, bitwise the same dx / dk as the split calls
+    # timed above, which give the per-path table).
+    fused_bwd = args.bwd == "fused" and peer is None and scheme == ks.HIERARCHICAL
+    fevs = None
+    if fused_bwd:
+        def run_bwd():
+            ks.backward(gy, x, k, mode, out=(dx, dk), workspace=ws)
+
+        bwd_fn = run_bwd
+        if graphs is not None:
+            gb = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gb):
+                run_bwd()
+            graphs.append(gb)
+            bwd_fn = gb.replay
+
+        def fstep(ev=None):
+            if ev:
+                ev[0].record(stream)
+            paths_fn[0]()
+            if ev:
+                ev[1].record(stream)
+            bwd_fn()
+            if ev:
+                ev[2].record(stream)
+            if comm is not None:
+                comm.allreduce_dw(dk)
+            if ev:
+                ev[3].record(stream)
+
+        for _ in range(args.warmup):
+            fstep()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        fevs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+        fstart = torch.cuda.Event(enable_timing=True)
+        fend = torch.cuda.Event(enable_timing=True)
+        fstart.record(stream)
+        for i in range(args.steps):
+            if flush is not None:
+                flush.fill_(float(i))
+            fstep(fevs[i])
+        fend.record(stream)
+        torch.cuda.synchronize()
     clk.__exit__(None, None, None)
     if world > 1:
         dist.barrier()
@@ -386,10 +435,15 @@ def run_ours(args, cfg_name, cfg):
     # the step is first path start -> combine end, summed over steps (flushes excluded)
     ms_total = start.elapsed_time(end) if flush is None else float(
         sum(e[0].elapsed_time(e[4]) for e in evs))
+    fper_mean = np.zeros(3)
+    if fused_bwd:
+        fper_mean = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in fevs]).mean(axis=0)
+        ms_total = fstart.elapsed_time(fend) if flush is None else float(
+            sum(e[0].elapsed_time(e[3]) for e in fevs))
     if world > 1:
-        t = torch.tensor([ms_total] + per_mean.tolist(), dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total] + per_mean.tolist() + fper_mean.tolist(), dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, per_mean = float(t[0]), t[1:].cpu().numpy()
+        ms_total, per_mean, fper_mean = float(t[0]), t[1:5].cpu().numpy(), t[5:8].cpu().numpy()
     ms_step = ms_total / args.steps
 
     if args.timing_log and rank == 0:
@@ -416,6 +470,17 @@ def run_ours(args, cfg_name, cfg):
                     "TFLOP_s_paper": round(fl, 2)}
     if world > 1:
         paths["dW_allreduce"] = {"ms": round(float(per_mean[3]), 4), "bytes": 4 * H * K}
+    if fused_bwd:
+        # logical bytes of the two paths it replaces vs the bytes it moves
+        # (fused kernel: read gy + x, write dx = 12 B per element; else 16)
+        fused_kernel = L % 32 == 0 and L >= 2048 and K <= 16
+        moved = (12 if fused_kernel else 16) * B * H * L + 8 * H * K
+        paths["bwd_fused"] = {"ms": round(float(fper_mean[1]), 4),
+                              "GB_s_logical": round(2 * pb / (fper_mean[1] * 1e-3) / 1e9, 1),
+                              "bytes_moved": moved,
+                              "GB_s_moved": round(moved / (fper_mean[1] * 1e-3) / 1e9, 1),
+                              "frac_hbm_measured": round(moved / (fper_mean[1] * 1e-3) / 1e9 / peak, 4),
+                              "fused_kernel": fused_kernel}
     dom = int(np.argmax(per_mean[:3]))
     traffic = ncu_traffic(cfg_name)
     dom_traffic = None
@@ -427,6 +492,17 @@ def run_ours(args, cfg_name, cfg):
                 "kernel": names[dom], "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": pb,
                 "note": "achieved = (8*B*H*L + 4*H*K) bytes / mean CUDA-event duration of the path"}
+    if fused_bwd and paths["bwd_fused"]["fused_kernel"] and fper_mean[1] > fper_mean[0]:
+        # the step's dominant kernel is the fused backward: its algorithmic
+        # (compulsory) bytes are read gy + x, write dx, read k, write dk
+        fb = paths["bwd_fused"]["bytes_moved"]
+        ach = fb / (fper_mean[1] * 1e-3) / 1e9
+        bt = traffic.get("bwd", {}).get("dram_bytes") if traffic else None
+        roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
+                    "frac": round(ach / peak, 4), "traffic": bt, "kernel": "bwd_fused (dX + dW, one pass)",
+                    "peak_kind": peak_kind, "algorithmic_bytes_per_launch": fb,
+                    "note": "achieved = (12*B*H*L + 8*H*K) compulsory bytes / mean CUDA-event duration; "
+                            "per-path split numbers in `paths`"}
     # long K is FP32-FMA-bound (paper arithmetic intensity K/4 FLOP/B above the
     # ridge): report against the FP32 roof measured in-process instead
     fp32 = C_double = None
@@ -450,6 +526,10 @@ def run_ours(args, cfg_name, cfg):
     # L % 32 == 0) or one conv_tile_f32; dW = stage 1 + the fixed-order
     # cross-block pass (hierarchical and pairwise alike)
     launches_per_step = (2 * 2 if L % 32 == 0 else 2) + 2
+    launches = launches_per_step * args.steps
+    if fused_bwd:  # the fused-step loop: fwd (2) + bwd (fused kernel + group sum, or the split 4)
+        fused_kernel = L % 32 == 0 and L >= 2048 and K <= 16
+        launches += ((2 if L % 32 == 0 else 1) + (2 if fused_kernel else launches_per_step - 2)) * args.steps
 
     # ---- end to end through the host-buffer C ABI (pinned host memory) ----
     e2e = None
@@ -527,9 +607,10 @@ def run_ours(args, cfg_name, cfg):
                        "mode": args.mode, "dw_scheme": args.scheme,
                        "l2": "inputs larger than L2 (no flush)" if flush is None
                              else "L2 flushed before every timed step (512 MB write, untimed)",
-                       "cuda_graphs": graphs is not None},
+                       "cuda_graphs": graphs is not None,
+                       "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)"},
             "paths": paths, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps,
+            "gpu_launches": launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
@@ -560,6 +641,8 @@ def main():
                     help="also write per-step path times in the reference's timing CSV schema")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch each path eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--bwd", choices=["fused", "split"], default="fused",
+                    help="step backward: one ks_dwconv1d_bwd_f32 call (dX + dW in one pass) or the two calls")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

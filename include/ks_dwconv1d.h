@@ -111,6 +111,19 @@ ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int6
                              int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                              int mode, void* ws, size_t ws_bytes, void* stream);
 
+/* The layer's whole backward in one call: dx = backward_input(gy, k) and
+ * dk = backward_weight(gy, x, HIERARCHICAL) -- the pair
+ * conv::backward_input (conv_core.hpp:56-59) + conv::backward_weight
+ * (:64-69) a training step makes back to back.  Where the fused kernel
+ * applies (K <= 16, L % 32 == 0, L >= 2048) gy and x are read from HBM once
+ * for both gradients (12 instead of 16 bytes moved per element); elsewhere
+ * the two kernels run in turn.  dx is bit-identical to ks_dwconv1d_dx_f32
+ * and dk to ks_dwconv1d_dw_f32(..., KS_DW_HIERARCHICAL, ...) in every case.
+ * ws / ws_bytes as for ks_dwconv1d_dw_f32 with KS_DW_HIERARCHICAL. */
+ks_status ks_dwconv1d_bwd_f32(const float* gy, const float* x, const float* k, float* dx, float* dk,
+                              int64_t B, int64_t H, int64_t L, int64_t K, int mode, void* ws,
+                              size_t ws_bytes, void* stream);
+
 /* On-device splitmix64 generator, bit-identical to the reference's
  * SplitMix64::next_pm1 (include/kernelscope/rng.hpp:12-28): out[i] = draw
  * (first+1+i) of the stream seeded with `seed`.  validate() draws x, then k,

@@ -29,7 +29,7 @@ EXPORTED = [
     "ks_status_string", "ks_last_error_string", "ks_abi_version",
     "ks_dwconv1d_fwd_f32", "ks_dwconv1d_fwd_f64", "ks_dwconv1d_dx_f32", "ks_dwconv1d_dx_f64",
     "ks_dwconv1d_dw_workspace_bytes", "ks_dwconv1d_dw_f32", "ks_dwconv1d_dw_f64",
-    "ks_fill_pm1_f32", "ks_probe_fp32_tflops",
+    "ks_dwconv1d_bwd_f32", "ks_fill_pm1_f32", "ks_probe_fp32_tflops",
     "ks_dwconv1d_fwd_f32_host", "ks_dwconv1d_dx_f32_host", "ks_dwconv1d_dw_f32_host",
     "ks_dwconv1d_fwd_f64_host", "ks_dwconv1d_dx_f64_host", "ks_dwconv1d_dw_f64_host",
     "ks_dwconv1d_step_f32_host",
@@ -50,6 +50,7 @@ _SIGS = {
     "ks_dwconv1d_dx_f64": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _p], _int),
     "ks_dwconv1d_dw_workspace_bytes": ([_i64, _i64, _i64, _i64, _int, _i64, _int, C.POINTER(_sz)], _int),
     "ks_dwconv1d_dw_f32": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _i64, _int, _p, _sz, _p], _int),
+    "ks_dwconv1d_bwd_f32": ([_p, _p, _p, _p, _p, _i64, _i64, _i64, _i64, _int, _p, _sz, _p], _int),
     "ks_dwconv1d_dw_f64": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _i64, _int, _p, _sz, _p], _int),
     "ks_fill_pm1_f32": ([_u64, _u64, _p, _i64, _p], _int),
     "ks_probe_fp32_tflops": ([C.POINTER(C.c_double)], _int),

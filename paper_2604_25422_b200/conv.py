@@ -163,6 +163,28 @@ def backward_weight(gy, x, K: int, scheme: int = SEQUENTIAL, chunk: int = 1024,
     return out
 
 
+def backward(gy, x, k, mode: int = SEPARATE, out=None, workspace=None):
+    """(dx, dk) = (conv::backward_input(gy, k), conv::backward_weight(gy, x,
+    HIERARCHICAL)) in one call (ks_dwconv1d_bwd_f32): the layer's backward,
+    fused so gy and x cross HBM once where the fused kernel applies.  Device
+    (torch CUDA) fp32 tensors; bits equal the two separate calls."""
+    B, H, L = _dims3(gy, "backward: gy")
+    _dims3(x, "backward: x", (B, H, L))
+    K = _dims_k(k, "backward: k", H)
+    if not _is_torch(gy) or _suffix(gy) != "f32" or _suffix(x) != "f32" or _suffix(k) != "f32":
+        raise TypeError("backward: fp32 CUDA tensors")
+    if out is None:
+        out = (_empty_like(gy, (B, H, L)), _empty_like(gy, (H, K)))
+    dx, dk = out
+    ws_ptr, ws_bytes = None, 0
+    if workspace is not None:
+        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    st = _lib.lib().ks_dwconv1d_bwd_f32(_ptr(gy), _ptr(x), _ptr(k), _ptr(dx), _ptr(dk), B, H, L, K, mode,
+                                        ws_ptr, ws_bytes, _stream(gy))
+    _raise_dims(st, "backward")
+    return dx, dk
+
+
 def step_host(x, k, gy, K: int | None = None, scheme: int = HIERARCHICAL, chunk: int = 0,
               mode: int = FUSED, out=None):
     """One fwd + dX + dW step on host (numpy) buffers through

@@ -20,6 +20,8 @@ ks_status dw_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, 
                  int64_t, int, void*, cudaStream_t);
 ks_status dw_f64(const double*, const double*, double*, int64_t, int64_t, int64_t, int64_t, int,
                  int64_t, int, void*, cudaStream_t);
+ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* dx, float* dk, int64_t B,
+                        int64_t H, int64_t L, int64_t K, int mode, void* ws, cudaStream_t st, bool* fused);
 
 size_t variant_workspace_bytes(int variant, int path, int64_t H, int64_t K);
 bool variant_supported(int variant, int path, int64_t B, int64_t H, int64_t L, int64_t K);
@@ -287,6 +289,22 @@ ks_status ks_dwconv1d_dw_f32(const float* gy, const float* x, float* dk, int64_t
     Scratch s;
     KS_TRY(s.take(ws, ws_bytes, dw_workspace_bytes(B, H, L, K, scheme, chunk, 4), st));
     return dw_f32(gy, x, dk, B, H, L, K, scheme, chunk, mode, s.ptr, st);
+}
+
+ks_status ks_dwconv1d_bwd_f32(const float* gy, const float* x, const float* k, float* dx, float* dk, int64_t B,
+                              int64_t H, int64_t L, int64_t K, int mode, void* ws, size_t ws_bytes, void* stream) {
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (!gy || !x || !k || !dx || !dk) return KS_ERR_NULL;
+    KS_TRY(check_device());
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Scratch s;
+    KS_TRY(s.take(ws, ws_bytes, dw_workspace_bytes(B, H, L, K, KS_DW_HIERARCHICAL, 0, 4), st));
+    bool fused = false;
+    KS_TRY(bwd_fused_f32(gy, x, k, dx, dk, B, H, L, K, mode, s.ptr, st, &fused));
+    if (fused) return KS_OK;
+    KS_TRY(ks_dwconv1d_dx_f32(gy, k, dx, B, H, L, K, mode, stream));
+    return dw_f32(gy, x, dk, B, H, L, K, KS_DW_HIERARCHICAL, 0, mode, s.ptr, st);
 }
 
 ks_status ks_dwconv1d_dw_f64(const double* gy, const double* x, double* dk, int64_t B, int64_t H,

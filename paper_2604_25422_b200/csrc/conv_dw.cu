@@ -529,6 +529,27 @@ ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B
     return s;
 }
 
+ks_status bwd_tma_stage1(const float*, const float*, const float*, float*, float*, int64_t, int64_t, int64_t,
+                         int64_t, int, int, cudaStream_t, bool*);
+
+// Fused backward (dx + HIERARCHICAL dk) where dw_f32 would run the TMA dW
+// kernel with one tap group (L % 32 == 0, L >= 2048, K <= 16): same row
+// groups G, same decomposition, so dk's bits equal dw_f32's and dx's equal
+// the stencil's.  *fused = false: the caller runs dX and dW in turn.
+ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* dx, float* dk, int64_t B,
+                        int64_t H, int64_t L, int64_t K, int mode, void* ws, cudaStream_t st, bool* fused) {
+    *fused = false;
+    if (tma_disabled() || L < 2048 || L % 32 != 0 || K > 16 || dw_cb_applies(B, H, L, K)) return KS_OK;
+    if (L > (1ll << 30) || B > (1ll << 30)) return KS_OK;
+    const HierPlan pl = hier_plan(B, H, K);
+    float* part = static_cast<float*>(ws);
+    const ks_status s = bwd_tma_stage1(gy, x, k, dx, part, B, H, L, K, pl.g, mode, st, fused);
+    if (s != KS_OK || !*fused) return s;
+    const int64_t HK = H * K;
+    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.g);
+    return check_launch();
+}
+
 ks_status dw_f64(const double* gy, const double* x, double* dk, int64_t B, int64_t H, int64_t L,
                  int64_t K, int scheme, int64_t chunk, int mode, void* ws, cudaStream_t st) {
     return dw_exact<double>(gy, x, dk, B, H, L, K, scheme, chunk, mode, ws, st);

@@ -36,7 +36,8 @@ constexpr int kDwMain = kDwTT / kDwIn;   // x window main-box rows
 struct DwGeomT {
     int XR;           // x window rows (32 floats): kDwMain main + XT tail
     int XT;           // tail rows
-    int gy_bytes;     // kDwTT*4
+    int gy_bytes;     // gy region in a stage (1024-aligned: 64 rows, or 72 when BWD stages a halo)
+    int gy_box;       // gy rows loaded per item (64, or 66 = tile + one halo row each side)
     int stage_bytes;
 };
 
@@ -48,18 +49,32 @@ __device__ __forceinline__ int block_t(int q) {
     else return ((q & 31) * 2 + ((q >> 5) & 1) + (q >> 6) * 64) * TB;
 }
 
-template <int JR, int TB, int NJ, int S, bool FUSED, bool PROD>
-__global__ void __launch_bounds__(kThreads + (PROD ? 32 : 0))
+// BWD = the fused backward: the same dW work (identical decomposition and
+// accumulation order, so dk is bit-identical to the dW-only kernel) plus dX
+// from the gy tile already in shared memory.  The gy box then carries one
+// 32-float halo row on each side (gy logical index 0 = t0 - 32); every thread
+// computes the 8 dX outputs of its own dW t-block (taps reversed, held in
+// registers, window sub-quad offset S2 = (-q) mod 4), writes them to a
+// swizzled output buffer, and thread 0 stores each 2048-wide tile with one
+// TMA tensor store (double-buffered).  gy and x are read from HBM once for
+// both gradients: 12 B per element instead of 16 (dX 8 + dW 8).
+template <int JR, int TB, int NJ, int S, bool FUSED, bool BWD, int S2>
+__global__ void __launch_bounds__(kThreads)
 dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUtensorMap x_map,
-       const __grid_constant__ CUtensorMap x_tail_map, float* __restrict__ part, int B, int H, int L, int K, int p,
-       int G, int NJT, DwGeomT g, int NS) {
+       const __grid_constant__ CUtensorMap x_tail_map, const __grid_constant__ CUtensorMap dx_map,
+       const float* __restrict__ k, float* __restrict__ part, int B, int H, int L, int K, int p, int G, int NJT,
+       DwGeomT g, int NS) {
     constexpr int NTS = kThreads / NJ;
     constexpr int JT = NJ * JR;
     constexpr int SPT = kDwTT / (NTS * TB);
     constexpr int NVX = (S + TB + JR - 1 + 3) / 4;
+    constexpr int NV2 = (S2 + TB + JR - 1 + 3) / 4;  // dX window quads (K <= JR)
+    constexpr int GOFS = BWD ? kDwIn : 0;            // gy logical index of t0
+    static_assert(!BWD || (NJ == 1 && TB == 8), "the fused backward needs one tap group of 8-wide blocks");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * g.stage_bytes);
+    unsigned char* outb = smem + NS * g.stage_bytes;  // BWD: 2 x 8 KB dX tiles
+    uint64_t* full = reinterpret_cast<uint64_t*>(outb + (BWD ? 2 * kDwTT * 4 : 0));
     __shared__ float red[kThreads / 32][JR];
 
     int bid = blockIdx.x;
@@ -81,46 +96,39 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int xr_rel = (xoff - D) / kDwIn;  // exact division
     const int A = D & ~3;                   // D & 3 == S
 
-    uint64_t* empty = full + NS;
     if (tid == 0) {
         prefetch_tmap(&gy_map);
         prefetch_tmap(&x_map);
         prefetch_tmap(&x_tail_map);
-        for (int s = 0; s < NS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kThreads);
-        }
+        if (BWD) prefetch_tmap(&dx_map);
+        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
 
-    const uint32_t tx_bytes = static_cast<uint32_t>(g.gy_bytes + g.XR * kDwIn * 4);
+    const uint32_t tx_bytes = static_cast<uint32_t>(g.gy_box * kDwIn * 4 + g.XR * kDwIn * 4);
     auto issue = [&](int stage, int u) {
         const int b = b_begin + u / ntt;
         const int t0 = (u % ntt) * kDwTT;
         const int row = b * H + h;
         unsigned char* sb = smem + stage * g.stage_bytes;
         mbar_arrive_expect_tx(&full[stage], tx_bytes);
-        tma_load_3d(sb, &gy_map, 0, t0 / kDwIn, row, &full[stage]);
+        tma_load_3d(sb, &gy_map, 0, t0 / kDwIn - (BWD ? 1 : 0), row, &full[stage]);
         const int xr = t0 / kDwIn + xr_rel;
         tma_load_3d(sb + g.gy_bytes, &x_map, 0, xr, row, &full[stage]);
         tma_load_3d(sb + g.gy_bytes + kDwMain * kDwIn * 4, &x_tail_map, 0, xr + kDwMain, row, &full[stage]);
     };
-    if constexpr (PROD) {
-        // producer warp: lane 0 keeps the ring NS items ahead; consumer
-        // threads release a stage as soon as they are done (no CTA barrier)
-        if (tid >= kThreads) {
-            if (tid == kThreads)
-                for (int u = 0; u < nunits; ++u) {
-                    const int stage = u % NS;
-                    if (u >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((u / NS - 1) & 1));
-                    issue(stage, u);
-                }
-            return;
-        }
-    } else {
-        if (tid == 0)
-            for (int s = 0; s < NS && s < nunits; ++s) issue(s, s);
+    if (tid == 0)
+        for (int s = 0; s < NS && s < nunits; ++s) issue(s, s);
+
+    // dX taps, reversed (the reference's k[h, K-1-j], src/conv_core.cpp:68), zero past K
+    float wr[BWD ? JR : 1];
+    int a2 = 0;
+    if constexpr (BWD) {
+#pragma unroll
+        for (int jj = 0; jj < JR; ++jj) wr[jj] = jj < K ? k[static_cast<int64_t>(h) * K + K - 1 - jj] : 0.f;
+        const int q = K - 1 - p;    // dX offset (src/conv_core.cpp:56)
+        a2 = GOFS - q - S2;         // 4-aligned gy index of a block's first dX tap, minus tl
     }
 
     float acc[JR];
@@ -132,6 +140,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         mbar_wait(&full[stage], static_cast<uint32_t>((u / NS) & 1));
         const unsigned char* gys = smem + stage * g.stage_bytes;
         const unsigned char* xs = gys + g.gy_bytes;
+        unsigned char* ob = outb + (u & 1) * kDwTT * 4;
         const int t0 = (u % ntt) * kDwTT;
 #pragma unroll 2
         for (int s = 0; s < SPT; ++s) {
@@ -140,7 +149,8 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 float gv[TB];
 #pragma unroll
                 for (int c = 0; c < TB / 4; ++c) {
-                    const float4 q = *reinterpret_cast<const float4*>(gys + swz<128>(static_cast<uint32_t>(tl + 4 * c)));
+                    const float4 q =
+                        *reinterpret_cast<const float4*>(gys + swz<128>(static_cast<uint32_t>(GOFS + tl + 4 * c)));
                     gv[4 * c + 0] = q.x;
                     gv[4 * c + 1] = q.y;
                     gv[4 * c + 2] = q.z;
@@ -160,15 +170,49 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 for (int tt = 0; tt < TB; ++tt)
 #pragma unroll
                     for (int jj = 0; jj < JR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+                if constexpr (BWD) {
+                    // dx[t0+tl+r] = sum_j gy[t0+tl+r+j-q] * k[K-1-j], j ascending from +0
+                    float v2[4 * NV2];
+                    const uint32_t gi = static_cast<uint32_t>(a2 + tl);
+#pragma unroll
+                    for (int c = 0; c < NV2; ++c) {
+                        const float4 q = *reinterpret_cast<const float4*>(gys + swz<128>(gi + 4 * c));
+                        v2[4 * c + 0] = q.x;
+                        v2[4 * c + 1] = q.y;
+                        v2[4 * c + 2] = q.z;
+                        v2[4 * c + 3] = q.w;
+                    }
+                    float d[TB];
+#pragma unroll
+                    for (int r = 0; r < TB; ++r) d[r] = 0.f;
+#pragma unroll
+                    for (int jj = 0; jj < JR; ++jj)
+                        if (jj < K) {
+#pragma unroll
+                            for (int r = 0; r < TB; ++r) d[r] = muladd<FUSED>(d[r], v2[S2 + r + jj], wr[jj]);
+                        }
+#pragma unroll
+                    for (int r = 0; r < TB; r += 4)
+                        *reinterpret_cast<float4*>(ob + swz<128>(static_cast<uint32_t>(tl + r))) =
+                            make_float4(d[r], d[r + 1], d[r + 2], d[r + 3]);
+                }
             }
         }
-        if constexpr (PROD) {
-            mbar_arrive(&empty[stage]);  // this thread is done with the stage
-        } else {
-            __syncthreads();
-            if (tid == 0 && u + NS < nunits) issue(stage, u + NS);
+        if constexpr (BWD) {
+            fence_proxy_async_smem();           // dX tile visible to the TMA store
+            if (tid == 0) bulk_wait_read_all();  // store u-1 has read buffer (u+1)&1
+        }
+        __syncthreads();
+        if (tid == 0) {
+            if constexpr (BWD) {
+                const int b = b_begin + u / ntt;
+                tma_store_3d(&dx_map, ob, 0, t0 / kDwIn, b * H + h);  // columns past L are clipped
+                bulk_commit();
+            }
+            if (u + NS < nunits) issue(stage, u + NS);
         }
     }
+    if (BWD && tid == 0) bulk_wait_all();
 
 #pragma unroll
     for (int jj = 0; jj < JR; ++jj) {
@@ -182,7 +226,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 #pragma unroll
         for (int jj = 0; jj < JR; ++jj) red[warp][jj] = acc[jj];
     }
-    asm volatile("bar.sync 1, %0;" ::"n"(kThreads) : "memory");  // the consumer warps
+    __syncthreads();
     constexpr int WPG = NTS / 32;  // warps per tap group
     if (tid < JT) {
         const int gj = tid / JR, jj = tid % JR;
@@ -194,51 +238,46 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     }
 }
 
-template <int JR, int TB, int NJ, bool FUSED, bool PROD>
-ks_status launch(int s, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt, float* part, int64_t B,
-                 int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
-    const int smem = NS * g.stage_bytes + 128 + 1024;
-    constexpr int threads = kThreads + (PROD ? 32 : 0);
+struct Maps {
+    CUtensorMap gm, xm, xt, dxm;
+};
+
+template <int JR, int TB, int NJ, bool FUSED, bool BWD>
+ks_status launch(int s, int s2, const Maps& mp, const float* k, float* part, int64_t B, int64_t H, int64_t L,
+                 int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
+    const int smem = NS * g.stage_bytes + (BWD ? 2 * kDwTT * 4 : 0) + 64 + 1024;
     const unsigned blocks = static_cast<unsigned>(int64_t(G) * H * NJT);
     const int p = static_cast<int>(K / 2);
-#define KS_DW_CASE(SV)                                                                                        \
-    case SV: {                                                                                                \
-        auto kern = dw_tma<JR, TB, NJ, SV, FUSED, PROD>;                                                      \
-        prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);                                 \
-        kern<<<blocks, threads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),       \
-                                             static_cast<int>(L), static_cast<int>(K), p, G, NJT, g, NS);     \
-        break;                                                                                                \
+#define KS_DW_CASE(SV, S2V)                                                                                    \
+    if (s == SV && s2 == S2V) {                                                                                \
+        auto kern = dw_tma<JR, TB, NJ, SV, FUSED, BWD, S2V>;                                                   \
+        prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                 \
+        kern<<<blocks, kThreads, smem, st>>>(mp.gm, mp.xm, mp.xt, mp.dxm, k, part, static_cast<int>(B),        \
+                                             static_cast<int>(H), static_cast<int>(L), static_cast<int>(K), p, \
+                                             G, NJT, g, NS);                                                   \
+        return check_launch();                                                                                 \
     }
-    switch (s) {
-        KS_DW_CASE(0)
-        KS_DW_CASE(1)
-        KS_DW_CASE(2)
-        default:
-        KS_DW_CASE(3)
+    if constexpr (BWD) {
+        // S2 = (-q) mod 4 with q = K-1-p: S2 = S for odd K, S + 1 (mod 4) for even K
+        KS_DW_CASE(0, 0) KS_DW_CASE(0, 1) KS_DW_CASE(1, 1) KS_DW_CASE(1, 2)
+        KS_DW_CASE(2, 2) KS_DW_CASE(2, 3) KS_DW_CASE(3, 3) KS_DW_CASE(3, 0)
+    } else {
+        KS_DW_CASE(0, 0) KS_DW_CASE(1, 0) KS_DW_CASE(2, 0) KS_DW_CASE(3, 0)
     }
 #undef KS_DW_CASE
-    return check_launch();
+    return KS_ERR_CUDA;
 }
 
-template <int JR, int TB, int NJ>
-ks_status launch_m(int s, bool fused, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& xt,
-                   float* part, int64_t B, int64_t H, int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS,
-                   cudaStream_t st) {
-    const char* e = getenv("KS_DWTMA_PROD");  // A/B knob: 1 = producer lane, no CTA barrier per item
-    if (e && atoi(e) == 1)
-        return fused ? launch<JR, TB, NJ, true, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
-                     : launch<JR, TB, NJ, false, true>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
-    return fused ? launch<JR, TB, NJ, true, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st)
-                 : launch<JR, TB, NJ, false, false>(s, gm, xm, xt, part, B, H, L, K, G, NJT, g, NS, st);
+template <int JR, int TB, int NJ, bool BWD>
+ks_status launch_m(int s, int s2, bool fused, const Maps& mp, const float* k, float* part, int64_t B, int64_t H,
+                   int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
+    return fused ? launch<JR, TB, NJ, true, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st)
+                 : launch<JR, TB, NJ, false, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st);
 }
 
-}  // namespace
-
-// Stage 1 of HIERARCHICAL dW through TMA into part[G,H,K] (G = the caller's row
-// groups; stage 2 is shared with the generic path).  *handled = false means
-// the shape is not supported here and the caller falls back.
-ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
-                        int G, int mode, cudaStream_t st, bool* handled) {
+// Shared by the dW-only and the fused backward entry points.
+ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx, float* part, int64_t B, int64_t H,
+                     int64_t L, int64_t K, int G, int mode, bool bwd, cudaStream_t st, bool* handled) {
     *handled = false;
     if (L % kDwIn != 0 || B * H >= (int64_t(1) << 31) || L >= (int64_t(1) << 30) || K >= (int64_t(1) << 30))
         return KS_OK;
@@ -251,31 +290,64 @@ ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B,
     const int JR = K <= 16 && !j16 ? 8 : 16;
     int nj = JR == 8 || j16 ? 1 : 2;
     while (nj < 8 && nj * JR < K) nj *= 2;
+    if (bwd && !(nj == 1 && (JR == 8 || j16))) return KS_OK;  // fused backward: one tap group, TB = 8
     const int njt = static_cast<int>((K + nj * JR - 1) / (nj * JR));
     if (int64_t(G) * H * njt >= (int64_t(1) << 31)) return KS_OK;
     DwGeomT g;
-    g.gy_bytes = kDwTT * 4;
+    g.gy_box = kDwMain + (bwd ? 2 : 0);
+    g.gy_bytes = (g.gy_box * kDwIn * 4 + 1023) / 1024 * 1024;
     g.XT = (nj * JR + 40 + kDwIn - 1) / kDwIn;  // covers D + JT + the register-window overrun
     g.XR = kDwMain + g.XT;
     g.stage_bytes = (g.gy_bytes + g.XR * kDwIn * 4 + 1023) / 1024 * 1024;
-    CUtensorMap gm, xm, xt;
-    if (!encode_row_view(&gm, gy, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
-    if (!encode_row_view(&xm, x, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
-    if (!encode_row_view(&xt, x, B * H, L, kDwIn, g.XT, 128)) return KS_OK;
+    Maps mp;
+    if (!encode_row_view(&mp.gm, gy, B * H, L, kDwIn, g.gy_box, 128)) return KS_OK;
+    if (!encode_row_view(&mp.xm, x, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+    if (!encode_row_view(&mp.xt, x, B * H, L, kDwIn, g.XT, 128)) return KS_OK;
+    if (bwd) {
+        if (!encode_row_view(&mp.dxm, dx, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+    } else {
+        mp.dxm = mp.gm;  // unused
+    }
     const int NS = std::max(2, std::min(4, (72 * 1024) / g.stage_bytes));
     const int p = static_cast<int>(K / 2);
     const int s = (4 - p % 4) % 4;
+    const int q = static_cast<int>(K) - 1 - p;
+    const int s2 = bwd ? (4 - q % 4) % 4 : 0;
     const bool fused = mode == KS_MULADD_FUSED;
     *handled = true;
-    if (j16) return launch_m<16, 8, 1>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+    if (bwd)
+        return j16 ? launch_m<16, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st)
+                   : launch_m<8, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+    if (j16) return launch_m<16, 8, 1, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     if (JR == 8)
-        return nj == 1 ? launch_m<8, 8, 1>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st)
-                       : launch_m<8, 8, 2>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+        return nj == 1 ? launch_m<8, 8, 1, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st)
+                       : launch_m<8, 8, 2, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     switch (nj) {
-        case 2: return launch_m<16, 16, 2>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
-        case 4: return launch_m<16, 16, 4>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
-        default: return launch_m<16, 16, 8>(s, fused, gm, xm, xt, part, B, H, L, K, G, njt, g, NS, st);
+        case 2: return launch_m<16, 16, 2, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        case 4: return launch_m<16, 16, 4, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        default: return launch_m<16, 16, 8, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     }
+}
+
+}  // namespace
+
+// Stage 1 of HIERARCHICAL dW through TMA into part[G,H,K] (G = the caller's row
+// groups; stage 2 is shared with the generic path).  *handled = false means
+// the shape is not supported here and the caller falls back.
+ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+                        int G, int mode, cudaStream_t st, bool* handled) {
+    return run_dw_tma(gy, x, nullptr, nullptr, part, B, H, L, K, G, mode, false, st, handled);
+}
+
+// Fused backward (dX + stage 1 of HIERARCHICAL dW) for K <= 16, L % 32 == 0:
+// dx is written in full, part[G,H,K] exactly as dw_tma_stage1 would write it.
+ks_status bwd_tma_stage1(const float* gy, const float* x, const float* k, float* dx, float* part, int64_t B,
+                         int64_t H, int64_t L, int64_t K, int G, int mode, cudaStream_t st, bool* handled) {
+    if (K > 16 || (reinterpret_cast<uintptr_t>(dx) & 15) != 0) {
+        *handled = false;
+        return KS_OK;
+    }
+    return run_dw_tma(gy, x, k, dx, part, B, H, L, K, G, mode, true, st, handled);
 }
 
 }  // namespace ks

@@ -67,8 +67,19 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
     return ("dw_tma" if L % 32 == 0 else "dw_hier_stage1"), G
 
 
+def bwd_fused_applies(L: int, K: int) -> bool:
+    """ks_dwconv1d_bwd_f32 runs the one-pass kernel (csrc/dw_tma.cu BWD)."""
+    return L % 32 == 0 and L >= 2048 and K <= 16
+
+
 def plan(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> dict:
-    """Kernel family, register tile / threads and tile geometry for a shape."""
+    """Kernel family, register tile / threads and tile geometry for a shape.
+    ``path`` is fwd, dx, dw or bwd (the fused backward entry point)."""
+    if path == "bwd":
+        if bwd_fused_applies(L, K):
+            _, G = _dw_groups(B, H, L, K)
+            return {"kernel": "dw_tma_bwd", "row_groups": G, "partials_bytes": 4 * G * H * K}
+        return {"kernel": "split", "dx": plan("dx", B, H, L, K), "dw": plan("dw", B, H, L, K)}
     if path in ("fwd", "dx"):
         name, R, NT = _stencil_tier(L, K)
         T = (NT or 0) * R if NT else None
@@ -82,6 +93,12 @@ def plan(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical"
 
 def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> int:
     """Modeled DRAM bytes per launch of the B200 kernels."""
+    if path == "bwd":
+        p = plan(path, B, H, L, K)
+        if p["kernel"] == "split":
+            return memory_traffic("dx", B, H, L, K) + memory_traffic("dw", B, H, L, K)
+        # one pass: read gy and x, write dx, read k; partials out and back
+        return 12 * B * H * L + 4 * H * K + 2 * p["partials_bytes"]
     base = logical_traffic(path, B, H, L, K)
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):

@@ -279,6 +279,43 @@ def test_padded_view_kernels_many_tiles(oracle, shape):
             assert normwise(dk[h:h + 1], truth) <= HIER_TOL
 
 
+@pytest.mark.parametrize("shape", [(3, 4, 2048, 7), (2, 3, 4096, 8), (5, 2, 2080, 16), (4, 3, 3072, 9),
+                                   (2, 2, 2048, 1), (16, 8, 2048, 13), (1, 1, 2048, 2), (40, 16, 2048, 7),
+                                   (2, 2, 1024, 7), (2, 2, 2048, 40)])
+def test_fused_backward_equals_separate_calls(shape):
+    """ks_dwconv1d_bwd_f32 (one pass over gy and x for dX and dW where the
+    fused kernel applies: K <= 16, L % 32 == 0, L >= 2048; the split calls
+    elsewhere) gives dx bitwise equal to backward_input and dk bitwise equal
+    to backward_weight(HIERARCHICAL), in both multiply-add modes.  Covers odd
+    and even K (both sub-quad offsets), K = 1, the 16-tap group, ragged last
+    tiles (L = 2080, 3072), several work items per CTA, and the fallbacks."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(9, B, H, L, K)
+    for m in (SEPARATE, FUSED):
+        dx, dk = ks.backward(gy, x, k, m)
+        assert same(host(dx), host(ks.backward_input(gy, k, m))), m
+        assert same(host(dk), host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))), m
+
+
+def test_fused_backward_config3_against_oracle(oracle):
+    """At config 3 (4 GiB per tensor): the fused backward's dx on sampled
+    channels bitwise against the oracle, dk to tolerance against fp64."""
+    B, H, L, K = 256, 512, 8192, 7
+    torch.cuda.empty_cache()
+    x, k, gy = ks.make_inputs(1, B, H, L, K)
+    dx, dk = ks.backward(gy, x, k, FUSED)
+    torch.cuda.synchronize()
+    kh = k.cpu().numpy()
+    for h in (0, H - 1):
+        xs, gs = _channel_slice(x, h), _channel_slice(gy, h)
+        ks_ = np.ascontiguousarray(kh[h:h + 1])
+        assert same(_channel_slice(dx, h), oracle.backward_input(gs, ks_, FUSED))
+        truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+        assert normwise(dk[h:h + 1].cpu().numpy(), truth) <= HIER_TOL
+    del x, gy, dx
+    torch.cuda.empty_cache()
+
+
 def test_full_config3_identities():
     """Adjoint <gy, fwd(x)> == <dX(gy), x> and pairing <gy, fwd(x)> ==
     sum(dk*k) at config 3 (4 GiB per tensor), in fp64 reductions."""

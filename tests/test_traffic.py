@@ -22,11 +22,20 @@ def test_plan_dispatch_tiers():
     assert traffic.plan("dw", 256, 512, 8192, 7, "pairwise")["kernel"] == "dw_pairwise_tma"
 
 
+def test_fused_backward_moves_three_quarters():
+    B, H, L, K = 256, 512, 8192, 7
+    assert traffic.plan("bwd", B, H, L, K)["kernel"] == "dw_tma_bwd"
+    assert traffic.plan("bwd", 64, 128, 4096, 4096)["kernel"] == "split"
+    split = traffic.memory_traffic("dx", B, H, L, K) + traffic.memory_traffic("dw", B, H, L, K)
+    assert abs(traffic.memory_traffic("bwd", B, H, L, K) / split - 0.75) < 0.01
+
+
 def test_model_matches_ncu_dram_bytes():
     with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
         meas = json.load(f)["config3"]
     B, H, L, K = 256, 512, 8192, 7
-    for path, key in (("fwd", "fwd"), ("dx", "dX"), ("dw", "dW")):
+    pairs = [("fwd", "fwd"), ("dx", "dX"), ("dw", "dW")] + ([("bwd", "bwd")] if "bwd" in meas else [])
+    for path, key in pairs:
         model = traffic.memory_traffic(path, B, H, L, K)
         got = meas[key]["dram_bytes"]
         assert abs(got - model) / model < 0.01, (path, got, model)

@@ -117,8 +117,26 @@ def main():
     if a.launches:
         per = launches(a.launches, a.round)
         # per-path DRAM bytes from the last complete fwd/dX/dW triple
+        def is_bwd(n):  # dw_tma<JR, TB, NJ, S, FUSED, BWD, S2>: the fused backward
+            if "dw_tma<" not in n:
+                return False
+            args = n.split("dw_tma<", 1)[1].split(">", 1)[0].split(",")
+            return len(args) >= 6 and args[5].strip() in ("1", "true")
+
         stencil = [m for (i, n, g, b), m in sorted(per.items()) if "stencil" in n or "conv_tile" in n]
-        dw = [m for (i, n, g, b), m in sorted(per.items()) if "dw_tma" in n or "dw_hier" in n]
+        dw = [m for (i, n, g, b), m in sorted(per.items())
+              if ("dw_tma" in n or "dw_hier" in n) and not is_bwd(n)]
+        bwd = [m for (i, n, g, b), m in sorted(per.items()) if is_bwd(n)]
+        if bwd:
+            m = bwd[-1]
+            cfg["bwd"] = {"dram_bytes": int(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]),
+                          "ncu_time_us": round(m["gpu__time_duration.sum"] / 1e3, 2), "round": a.round}
+        # with the fused-backward step the list ends ... fwd, dX, dW | fwd, bwd:
+        # take fwd and dX from the last split step (the stencils before the last dW)
+        if bwd and dw:
+            last_dw = max(i for (i, n, g, b) in per if ("dw_tma" in n or "dw_hier" in n) and not is_bwd(n))
+            stencil = [m for (i, n, g, b), m in sorted(per.items())
+                       if ("stencil" in n or "conv_tile" in n) and i < last_dw]
         if len(stencil) >= 2:
             for name, m in (("fwd", stencil[-2]), ("dX", stencil[-1])):
                 cfg[name] = {"dram_bytes": int(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]),
