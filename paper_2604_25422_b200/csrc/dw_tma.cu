@@ -308,7 +308,10 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
     } else {
         mp.dxm = mp.gm;  // unused
     }
-    const int NS = std::max(2, std::min(4, (72 * 1024) / g.stage_bytes));
+    int NS = std::max(2, std::min(4, (72 * 1024) / g.stage_bytes));
+    if (const char* e = getenv("KS_DWTMA_NS")) {  // tuning knob
+        if (atoi(e) >= 1 && atoi(e) <= 6) NS = atoi(e);
+    }
     const int p = static_cast<int>(K / 2);
     const int s = (4 - p % 4) % 4;
     const int q = static_cast<int>(K) - 1 - p;
