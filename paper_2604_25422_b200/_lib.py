@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libks_dwconv1d.so")
+# KS_LIB: an alternate build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("KS_LIB") or os.path.join(HERE, "libks_dwconv1d.so")
 
 # enums (include/ks_dwconv1d.h)
 KS_OK = 0

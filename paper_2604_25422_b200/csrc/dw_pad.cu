@@ -116,7 +116,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 float gv[kTW];
 #pragma unroll
                 for (int q = 0; q < kTW / 4; ++q) {
-                    const float4 a = *reinterpret_cast<const float4*>(gb + sub + 4 * q + (((sub + 4 * q) >> 5) << 2));
+                    const float4 a = lds4(gb + sub + 4 * q + (((sub + 4 * q) >> 5) << 2));
                     gv[4 * q + 0] = a.x;
                     gv[4 * q + 1] = a.y;
                     gv[4 * q + 2] = a.z;
@@ -125,7 +125,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 float xv[4 * kNVX];
 #pragma unroll
                 for (int q = 0; q < kNVX; ++q) {
-                    const float4 a = *reinterpret_cast<const float4*>(xb + sub + 4 * q + (((sub + 4 * q) >> 5) << 2));
+                    const float4 a = lds4(xb + sub + 4 * q + (((sub + 4 * q) >> 5) << 2));
                     xv[4 * q + 0] = a.x;
                     xv[4 * q + 1] = a.y;
                     xv[4 * q + 2] = a.z;

@@ -79,7 +79,7 @@ __device__ __forceinline__ void seg_tree(const unsigned char* gys, const unsigne
         float gv[8];
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
-            const float4 q = *reinterpret_cast<const float4*>(gys + swz<128>(tl + 4 * c));
+            const float4 q = lds4(gys + swz<128>(tl + 4 * c));
             gv[4 * c + 0] = q.x;
             gv[4 * c + 1] = q.y;
             gv[4 * c + 2] = q.z;
@@ -89,7 +89,7 @@ __device__ __forceinline__ void seg_tree(const unsigned char* gys, const unsigne
         const uint32_t xi = static_cast<uint32_t>(A) + tl + static_cast<uint32_t>(jgbase);
 #pragma unroll
         for (int c = 0; c < NVX; ++c) {
-            const float4 q = *reinterpret_cast<const float4*>(xs + swz<128>(xi + 4 * c));
+            const float4 q = lds4(xs + swz<128>(xi + 4 * c));
             xv[4 * c + 0] = q.x;
             xv[4 * c + 1] = q.y;
             xv[4 * c + 2] = q.z;

@@ -150,7 +150,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 #pragma unroll
                 for (int c = 0; c < TB / 4; ++c) {
                     const float4 q =
-                        *reinterpret_cast<const float4*>(gys + swz<128>(static_cast<uint32_t>(GOFS + tl + 4 * c)));
+                        lds4(gys + swz<128>(static_cast<uint32_t>(GOFS + tl + 4 * c)));
                     gv[4 * c + 0] = q.x;
                     gv[4 * c + 1] = q.y;
                     gv[4 * c + 2] = q.z;
@@ -160,7 +160,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 const uint32_t xi = static_cast<uint32_t>(A + tl + jg * JR);
 #pragma unroll
                 for (int c = 0; c < NVX; ++c) {
-                    const float4 q = *reinterpret_cast<const float4*>(xs + swz<128>(xi + 4 * c));
+                    const float4 q = lds4(xs + swz<128>(xi + 4 * c));
                     xv[4 * c + 0] = q.x;
                     xv[4 * c + 1] = q.y;
                     xv[4 * c + 2] = q.z;
@@ -176,7 +176,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                     const uint32_t gi = static_cast<uint32_t>(a2 + tl);
 #pragma unroll
                     for (int c = 0; c < NV2; ++c) {
-                        const float4 q = *reinterpret_cast<const float4*>(gys + swz<128>(gi + 4 * c));
+                        const float4 q = lds4(gys + swz<128>(gi + 4 * c));
                         v2[4 * c + 0] = q.x;
                         v2[4 * c + 1] = q.y;
                         v2[4 * c + 2] = q.z;

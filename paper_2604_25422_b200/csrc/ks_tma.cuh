@@ -25,6 +25,19 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
 
+// 128-bit shared load the compiler cannot narrow.  When only some lanes of a
+// window's last float4 are used, nvcc otherwise splits it into LDS.64 / LDS,
+// whose 8- / 4-byte accesses at a 128-byte (or 144-byte) lane stride
+// conflict 2- / 4-way where the full 16-byte access is conflict-free.
+// volatile: keeps the load after the stage's mbarrier wait.
+__device__ __forceinline__ float4 lds4(const void* p) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "r"(static_cast<uint32_t>(__cvta_generic_to_shared(p))));
+    return v;
+}
+
 // Pointer into the dynamic shared buffer rounded up to `align` bytes, derived
 // from the __shared__ array itself so the compiler keeps the shared address
 // space (LDS/STS rather than generic LD/ST).

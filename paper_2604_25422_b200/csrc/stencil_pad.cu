@@ -65,7 +65,7 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
         float v[4 * NV];
 #pragma unroll
         for (int c = 0; c < NV; ++c) {
-            const float4 q = *reinterpret_cast<const float4*>(base + sub + 4 * c + (((sub + 4 * c) >> 5) << 2));
+            const float4 q = lds4(base + sub + 4 * c + (((sub + 4 * c) >> 5) << 2));
             v[4 * c + 0] = q.x;
             v[4 * c + 1] = q.y;
             v[4 * c + 2] = q.z;

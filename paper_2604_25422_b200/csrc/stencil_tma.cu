@@ -125,7 +125,7 @@ stencil_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ 
                 const uint32_t i0 = static_cast<uint32_t>(base + g.A + j0);
 #pragma unroll
                 for (int c = 0; c < NV; ++c) {
-                    const float4 q = *reinterpret_cast<const float4*>(win + swz<SW>(i0 + 4 * c));
+                    const float4 q = lds4(win + swz<SW>(i0 + 4 * c));
                     v[4 * c + 0] = q.x;
                     v[4 * c + 1] = q.y;
                     v[4 * c + 2] = q.z;

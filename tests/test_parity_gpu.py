@@ -52,6 +52,8 @@ SHAPES = [(1, 1, 3, 3), (2, 3, 17, 5), (2, 2, 5, 4), (3, 2, 33, 8), (2, 2, 10, 1
           (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256), (4, 4, 4096, 16), (3, 2, 2048, 11),
           # short rows (rows_short.cu), incl. the paper's (L,K) = (48,48) and K > L
           (16, 8, 48, 48), (5, 3, 100, 9), (2, 3, 512, 64), (3, 2, 1020, 5), (7, 5, 96, 97), (70, 3, 48, 48),
+          # channel-major short rows (stencil_chan: L <= 128): partial batch groups, partial segments, K > L
+          (33, 4, 128, 5), (40, 3, 52, 33), (65, 2, 48, 1), (3, 7, 124, 130),
           # compute-bound dW (dw_pad.cu): K >= 128, ragged tap tiles, odd p (shifted tap origin)
           (2, 3, 2048, 130), (1, 2, 4096, 200), (3, 1, 6144, 555)]
 
