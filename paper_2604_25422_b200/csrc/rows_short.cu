@@ -25,7 +25,6 @@
 //   tree over rows, a fixed pass over t phases, one partial per CTA, and the
 //   shared fixed-order cross-block pass (dw_sum_groups).  No atomics.
 #include <algorithm>
-#include <cstdlib>
 
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
@@ -293,174 +292,14 @@ dw_rows(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUte
     }
 }
 
-// stencil_chan: channel-major chunks for short rows (L <= 128).  A stage
-// holds the 32 batch rows b0..b0+31 of ONE channel h (3-D view {L, H, B},
-// box {BOX, 1, 32}) plus that channel's tap row (1-D bulk copy), so all lanes
-// of a warp share one tap row -- tap loads are broadcasts -- while their
-// windows sit BOX (= 4 mod 32) floats apart: conflict-free 128-bit reads.
-// Warp w computes outputs [16w, 16w+16) of its lane's row with 16-tap
-// register blocks (ceil((S+31)/4) window loads + 4 broadcast tap loads per
-// 256 FMAs).  stencil_rows (rows of consecutive channels, one tap row per
-// lane) needs ~1 shared wavefront per 4 FMAs and saturates the LSU pipe at
-// the paper's (L, K) = (48, 48).  Accumulation is the reference's
-// ascending-j chain from +0 per output, bit-identical as everywhere else.
-constexpr int kJC = 16;  // taps per register block
-
-template <int S, bool FUSED>
-__global__ void __launch_bounds__(256)
-stencil_chan(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out,
-             int B, int H, int L, int K, int off, int nchunks, int BOX, int KP, int NS) {
-    constexpr int NV = (S + kR + kJC - 1 + 3) / 4;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    float* sm = reinterpret_cast<float*>(align_smem<128>(smem_raw));
-    const int stage_f = 32 * BOX + KP;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sm + NS * stage_f + 64);  // 64 floats of read slack
-    const int tid = threadIdx.x, lane = tid & 31, seg = tid >> 5;
-
-    if (tid == 0) {
-        prefetch_tmap(&in_map);
-        for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-    auto issue = [&](int stage, int c) {
-        const int bg = c / H, h = c - bg * H;
-        float* sb = sm + stage * stage_f;
-        mbar_arrive_expect_tx(&full[stage], static_cast<uint32_t>(stage_f) * 4u);
-        // innermost box coordinates must be 16-byte aligned: start S floats early
-        tma_load_3d(sb, &in_map, -off - S, h, bg * 32, &full[stage]);
-        bulk_load(sb + 32 * BOX, kp + static_cast<int64_t>(h) * KP, static_cast<uint32_t>(KP) * 4u, &full[stage]);
-    };
-    if (tid == 0)
-        for (int s = 0; s < NS; ++s)
-            if (static_cast<int>(blockIdx.x) + s * static_cast<int>(gridDim.x) < nchunks)
-                issue(s, blockIdx.x + s * gridDim.x);
-
-    const int Kfull = K - K % kJC;
-    const int ts = seg * kR;
-    int it = 0;
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
-        const int stage = it % NS;
-        mbar_wait(&full[stage], static_cast<uint32_t>((it / NS) & 1));
-        const float* sb = sm + stage * stage_f;
-        const float* xr = sb + lane * BOX + ts;  // box column S + t + j  <->  in[t + j - off]
-        const float* kr = sb + 32 * BOX;
-        float acc[kR];
-#pragma unroll
-        for (int r = 0; r < kR; ++r) acc[r] = 0.f;
-        auto block = [&](int j0, int nj) {
-            float v[4 * NV];
-#pragma unroll
-            for (int u = 0; u < NV; ++u) {
-                const float4 a = lds4(xr + j0 + 4 * u);
-                v[4 * u + 0] = a.x;
-                v[4 * u + 1] = a.y;
-                v[4 * u + 2] = a.z;
-                v[4 * u + 3] = a.w;
-            }
-            float w[kJC];
-#pragma unroll
-            for (int u = 0; u < kJC / 4; ++u) {
-                const float4 a = *reinterpret_cast<const float4*>(kr + j0 + 4 * u);
-                w[4 * u + 0] = a.x;
-                w[4 * u + 1] = a.y;
-                w[4 * u + 2] = a.z;
-                w[4 * u + 3] = a.w;
-            }
-#pragma unroll
-            for (int jj = 0; jj < kJC; ++jj)
-                if (jj < nj) {
-#pragma unroll
-                    for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[S + r + jj], w[jj]);
-                }
-        };
-        for (int j0 = 0; j0 < Kfull; j0 += kJC) block(j0, kJC);
-        if (Kfull < K) block(Kfull, K - Kfull);
-        __syncthreads();  // stage consumed
-        const int nc = c + NS * static_cast<int>(gridDim.x);
-        if (tid == 0 && nc < nchunks) issue(stage, nc);
-        const int bg = c / H, h = c - bg * H, b = bg * 32 + lane;
-        if (b < B && ts < L) {
-            float* o = out + (static_cast<int64_t>(b) * H + h) * L + ts;
-            if (ts + kR <= L) {
-#pragma unroll
-                for (int r = 0; r < kR; r += 4) st_cs_v4(o + r, make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]));
-            } else {
-#pragma unroll
-                for (int r = 0; r < kR; ++r)
-                    if (ts + r < L) o[r] = acc[r];
-            }
-        }
-    }
-}
-
 }  // namespace
 
-__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
-
-// Channel-major short-row stencil (stencil_chan); *handled = false outside
-// its envelope (L <= 128, L % 4 == 0).
-static ks_status stencil_chan_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L,
-                                  int64_t K, int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
-    *handled = false;
-    const char* e = getenv("KS_ROWS_CHAN");  // A/B knob: 0 = stencil_rows
-    if (e && *e == '0') return KS_OK;
-    if (L % 4 != 0 || L > 128 || K > 4096 || B >= (int64_t(1) << 31) || H >= (int64_t(1) << 30)) return KS_OK;
-    const int sh = static_cast<int>((4 - off % 4) % 4);
-    const int BOX = stride4(static_cast<int>(L + K) - 1 + sh);
-    if (BOX > 256) return KS_OK;
-    const int KP = round_up_i(static_cast<int>(K), kJC);
-    const int segs = static_cast<int>((L + kR - 1) / kR);
-    const int threads = 32 * segs;
-    const int stage_f = 32 * BOX + KP;
-    int NS = 4;
-    auto smem_of = [&](int ns) { return (int64_t(ns) * stage_f + 64) * 4 + 64 + 128; };
-    while (NS > 2 && smem_of(NS) > 72 * 1024) --NS;
-    const int64_t smem = smem_of(NS);
-    if (smem > 200 * 1024) return KS_OK;
-    const int64_t nchunks = (B + 31) / 32 * H;
-    if (nchunks >= (int64_t(1) << 31)) return KS_OK;
-    CUtensorMap im;
-    const cuuint64_t dims[3] = {static_cast<cuuint64_t>(L), static_cast<cuuint64_t>(H), static_cast<cuuint64_t>(B)};
-    const cuuint32_t box[3] = {static_cast<cuuint32_t>(BOX), 1, 32};
-    if (!encode_rows(&im, in, 3, dims, box)) return KS_OK;
-    float* kp = nullptr;
-    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * KP, st));
-    if (rc != KS_OK) return rc;
-    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * KP + 255) / 256, 4096)), 256, 0, st>>>(
-        k, kp, H, K, KP, reverse, 0);
-    rc = check_launch();
-    if (rc == KS_OK) {
-        const bool fused = mode == KS_MULADD_FUSED;
-        auto kern = fused ? stencil_chan<0, true> : stencil_chan<0, false>;
-        switch (sh) {
-            case 1: kern = fused ? stencil_chan<1, true> : stencil_chan<1, false>; break;
-            case 2: kern = fused ? stencil_chan<2, true> : stencil_chan<2, false>; break;
-            case 3: kern = fused ? stencil_chan<3, true> : stencil_chan<3, false>; break;
-            default: break;
-        }
-        const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), threads, static_cast<int>(smem));
-        const int64_t grid = std::min<int64_t>(nchunks, int64_t(num_sms()) * per_sm);
-        kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(im, kp, out, static_cast<int>(B),
-                                                                 static_cast<int>(H), static_cast<int>(L),
-                                                                 static_cast<int>(K), static_cast<int>(off),
-                                                                 static_cast<int>(nchunks), BOX, KP, NS);
-        rc = check_launch();
-    }
-    scratch_free(kp, st);
-    *handled = true;
-    return rc;
-}
-
+// fwd / dX for short rows; *handled = false outside the envelope.
 ks_status stencil_rows_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
                            int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
     if (L % 4 != 0 || B * H >= (int64_t(1) << 31)) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(in) & 15) || (reinterpret_cast<uintptr_t>(out) & 15)) return KS_OK;
-    {
-        const ks_status sc = stencil_chan_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
-        if (*handled) return sc;
-    }
     RowsGeom g;
     // box columns cover every tap of every output; register windows may read a
     // few floats past a row, which land in the next row / the tap area and only

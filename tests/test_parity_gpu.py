@@ -52,7 +52,6 @@ SHAPES = [(1, 1, 3, 3), (2, 3, 17, 5), (2, 2, 5, 4), (3, 2, 33, 8), (2, 2, 10, 1
           (1, 2, 2048, 20), (1, 1, 16384, 1024), (3, 1, 2048, 256), (4, 4, 4096, 16), (3, 2, 2048, 11),
           # short rows (rows_short.cu), incl. the paper's (L,K) = (48,48) and K > L
           (16, 8, 48, 48), (5, 3, 100, 9), (2, 3, 512, 64), (3, 2, 1020, 5), (7, 5, 96, 97), (70, 3, 48, 48),
-          # channel-major short rows (stencil_chan: L <= 128): partial batch groups, partial segments, K > L
           (33, 4, 128, 5), (40, 3, 52, 33), (65, 2, 48, 1), (3, 7, 124, 130),
           # compute-bound dW (dw_pad.cu): K >= 128, ragged tap tiles, odd p (shifted tap origin)
           (2, 3, 2048, 130), (1, 2, 4096, 200), (3, 1, 6144, 555)]
@@ -316,6 +315,26 @@ def test_fused_backward_config3_against_oracle(oracle):
         assert normwise(dk[h:h + 1].cpu().numpy(), truth) <= HIER_TOL
     del x, gy, dx
     torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("shape", [(2048, 64, 48, 48), (1000, 24, 96, 9)])
+def test_short_rows_many_chunks(oracle, shape):
+    """Short-row kernels with many chunks per CTA (every stage of the ring
+    reused): sampled channels bitwise (y, dX) in both modes, dW to tolerance."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(4, B, H, L, K)
+    kh = k.cpu().numpy()
+    for m in (SEPARATE, FUSED):
+        y = ks.forward(x, k, m)
+        dx = ks.backward_input(gy, k, m)
+        dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
+        for h in (0, H // 2, H - 1):
+            xs, gs = _channel_slice(x, h), _channel_slice(gy, h)
+            ks_ = np.ascontiguousarray(kh[h:h + 1])
+            assert same(_channel_slice(y, h), oracle.forward(xs, ks_, m)), (h, m)
+            assert same(_channel_slice(dx, h), oracle.backward_input(gs, ks_, m)), (h, m)
+            truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+            assert normwise(dk[h:h + 1], truth) <= HIER_TOL
 
 
 def test_full_config3_identities():
