@@ -41,12 +41,16 @@ for (B, H, L, K) in shapes:
 # items per CTA, so every stage ring slot and both mbarrier phases recur:
 # (32,64,2048,64) -> 1024 fwd/dX tiles over <= 444 CTAs; (32,256,2048,128) ->
 # 4 dW work items per CTA (> NS = 3 stages); odd p (K = 150) shifts the tap origin
-for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150)]:
+# (64,32,4096,7): fused backward (dX + dW in one pass), several work items per CTA
+# (2400,16,48,48): short-row chunks reused round the stage ring (paper shape rows)
+for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48)]:
     x, k, gy = o.fill_inputs(5, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
     y = ks.forward(dx_, dk_, 1)
     d = ks.backward_input(dgy, dk_, 1)
     dk = ks.backward_weight(dgy, dx_, K, ks.HIERARCHICAL, 0, 1)
+    if L % 32 == 0 and L >= 2048 and K <= 16:
+        ks.backward(dgy, dx_, dk_, 1)
     torch.cuda.synchronize()
     xs = np.ascontiguousarray(x[:, :1])
     gs = np.ascontiguousarray(gy[:, :1])
