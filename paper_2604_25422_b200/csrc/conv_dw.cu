@@ -63,7 +63,8 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
     const int tid = threadIdx.x;
     const int jg = tid / Geo::NTS;
     const int ts = tid - jg * Geo::NTS;
-    const bool vec_ok = (L & 3) == 0;
+    // 128-bit loads need 16-byte aligned rows (L % 4 == 0, aligned bases)
+    const bool vec_ok = (L & 3) == 0 && ((reinterpret_cast<uintptr_t>(gy) | reinterpret_cast<uintptr_t>(x)) & 15) == 0;
 
     float acc[kJR];
 #pragma unroll

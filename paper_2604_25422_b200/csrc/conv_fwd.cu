@@ -72,7 +72,10 @@ conv_tile_f32(const float* __restrict__ in, const float* __restrict__ k, float* 
         wk[j] = v;
     }
     // ---- stage the input window with a zero halo ----
-    const bool vec_ok = (L & 3) == 0;
+    // (128-bit global accesses need 16-byte aligned rows: L % 4 == 0 and
+    // 16-byte aligned base pointers -- callers may pass any float views)
+    const bool vec_ok = (L & 3) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0;
+    const bool vec_out = (L & 3) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     for (int c = tid; c < WL / 4; c += kTileThreads) {
         const int g = a0 + 4 * c;
         float4 v;
@@ -128,7 +131,7 @@ conv_tile_f32(const float* __restrict__ in, const float* __restrict__ k, float* 
     if (Kfull < K) block(Kfull, K - Kfull);
 
     float* rout = out + row * static_cast<int64_t>(L) + t0 + base;
-    if (vec_ok && t0 + base + R <= L) {
+    if (vec_out && t0 + base + R <= L) {
 #pragma unroll
         for (int r = 0; r < R; r += 4)
             st_cs_v4(rout + r, make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]));

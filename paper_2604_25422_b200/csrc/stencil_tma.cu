@@ -235,8 +235,10 @@ static void pick_tile(int64_t L, int64_t K, int* R, int* NT) {
         *R = 32;
         *NT = L >= 8192 ? 256 : L >= 4096 ? 128 : 64;
     } else if (L >= 1024) {
+        // K > 8 does twice the FMAs per byte: 128-thread CTAs (more of them
+        // per SM) hide it better (config 5a fwd 12.3 -> 11.4 ms)
         *R = 16;
-        *NT = L >= 4096 ? 256 : L >= 2048 ? 128 : 64;
+        *NT = L >= 4096 && K <= 8 ? 256 : L >= 2048 ? 128 : 64;
     } else {
         *R = 4;
         *NT = 256;
@@ -298,8 +300,9 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     if (!tma_out) om = im;  // unused
     const int s = static_cast<int>((4 - off % 4) % 4);
     // memory-bound tiles: 3 stages x 2 CTAs/SM measured best on config 3 (a
-    // sweep of NT in {128,256} x NS in {2,3,4,6,8} spans 5.9-6.3 TB/s)
-    int NS = 3;
+    // sweep of NT in {128,256} x NS in {2,3,4,6,8} spans 5.9-6.3 TB/s); 2
+    // stages of 128-thread tiles for K > 8 (config 5a)
+    int NS = K > 8 ? 2 : 3;
     while (NS > 2 && stencil_smem_bytes(g, NS, tma_out) > 110 * 1024) --NS;
     if (R == 32) {
         // compute-bound: spend shared memory on resident warps rather than deep

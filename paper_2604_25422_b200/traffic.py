@@ -43,7 +43,7 @@ def _stencil_tier(L: int, K: int):
     if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
     if L >= 1024:
-        nt = 256 if L >= 4096 else 128 if L >= 2048 else 64
+        nt = 256 if L >= 4096 and K <= 8 else 128 if L >= 2048 else 64
         return "stencil_tma", 16, nt
     return "stencil_tma", 4, 256
 

@@ -337,6 +337,37 @@ def test_short_rows_many_chunks(oracle, shape):
             assert normwise(dk[h:h + 1], truth) <= HIER_TOL
 
 
+@pytest.mark.parametrize("shape", [(2, 3, 4096, 7), (2, 2, 2048, 64), (2, 2, 2048, 200), (3, 2, 48, 48)])
+def test_unaligned_pointers_fall_back_correctly(oracle, shape):
+    """Tensors starting 4 bytes past a 16-byte boundary (TMA needs 16-byte
+    aligned bases): every entry point still returns the reference's bits
+    (y, dX) / the tolerance (dW), through the generic kernels."""
+    B, H, L, K = shape
+    x, k, gy = oracle.fill_inputs(6, B, H, L, K)
+
+    def shifted(a):  # a view whose data pointer is 4 bytes off 16-byte alignment
+        buf = torch.empty(a.size + 4, dtype=torch.float32, device="cuda")
+        v = buf[1:1 + a.size].view(a.shape)
+        v.copy_(torch.from_numpy(np.ascontiguousarray(a)))
+        return v
+
+    xs, gys, ks_ = shifted(x), shifted(gy), shifted(k)
+    assert xs.data_ptr() % 16 == 4
+    for m in (SEPARATE, FUSED):
+        y = shifted(np.zeros((B, H, L), np.float32))
+        ks.forward(xs, ks_, m, out=y)
+        assert same(host(y), oracle.forward(x, k, m)), m
+        dx = shifted(np.zeros((B, H, L), np.float32))
+        ks.backward_input(gys, ks_, m, out=dx)
+        assert same(host(dx), oracle.backward_input(gy, k, m)), m
+        dk = host(ks.backward_weight(gys, xs, K, ks.HIERARCHICAL, 0, m))
+        truth = oracle.backward_weight(gy.astype(np.float64), x.astype(np.float64), K, SEQUENTIAL)
+        assert normwise(dk, truth) <= HIER_TOL
+        dx2, dk2 = ks.backward(gys, xs, ks_, m)
+        assert same(host(dx2), oracle.backward_input(gy, k, m)), m
+        assert normwise(host(dk2), truth) <= HIER_TOL
+
+
 def test_full_config3_identities():
     """Adjoint <gy, fwd(x)> == <dX(gy), x> and pairing <gy, fwd(x)> ==
     sum(dk*k) at config 3 (4 GiB per tensor), in fp64 reductions."""
