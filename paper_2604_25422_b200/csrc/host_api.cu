@@ -12,6 +12,7 @@
 // association order, so the inputs are uploaded (two streams, one per tensor)
 // and the device entry point runs once; only dk[H,K] comes back.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ks_common.cuh"
@@ -20,7 +21,15 @@ namespace ks {
 
 namespace {
 
-constexpr size_t kBlockBytes = size_t(64) << 20;  // target bytes per streamed block
+// target bytes per streamed block (tuning knob KS_HOST_BLOCK_MB)
+size_t block_bytes() {
+    static const size_t b = [] {
+        const char* e = getenv("KS_HOST_BLOCK_MB");
+        const long mb = e ? atol(e) : 64;
+        return size_t(mb >= 1 && mb <= 4096 ? mb : 64) << 20;
+    }();
+    return b;
+}
 constexpr int kSlots = 3;
 
 struct DevicePool {
@@ -47,7 +56,7 @@ ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t
     if (!in || !k || !out) return KS_ERR_NULL;
     ensure_pool();
     const size_t entry = sizeof(T) * size_t(H) * size_t(L);  // one batch entry
-    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(kBlockBytes / std::max<size_t>(entry, 1))));
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(block_bytes() / std::max<size_t>(entry, 1))));
     const int64_t nblocks = (B + nb - 1) / nb;
     const int slots = static_cast<int>(std::min<int64_t>(kSlots, nblocks));
 
@@ -163,7 +172,7 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
     ensure_pool();
     const size_t entry = sizeof(float) * size_t(H) * size_t(L);
     const size_t tbytes = entry * size_t(B);
-    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(kBlockBytes / std::max<size_t>(entry, 1))));
+    const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(block_bytes() / std::max<size_t>(entry, 1))));
     const int64_t nblocks = (B + nb - 1) / nb;
     const int slots = static_cast<int>(std::min<int64_t>(kSlots, nblocks));
     cudaStream_t st[kSlots] = {};
@@ -171,11 +180,15 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
     float* dy[kSlots] = {};
     float* ddx[kSlots] = {};
     cudaEvent_t ev[kSlots] = {};
+    cudaEvent_t up[kSlots] = {};  // per stream: its latest block upload has landed
+    cudaStream_t sdw = nullptr;   // dW (and dk's download) overlap the trailing downloads
     ks_status rc = KS_OK;
     for (int s = 0; s < slots && rc == KS_OK; ++s) {
         rc = cuda_status(cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking));
         if (rc == KS_OK) rc = cuda_status(cudaEventCreateWithFlags(&ev[s], cudaEventDisableTiming));
+        if (rc == KS_OK) rc = cuda_status(cudaEventCreateWithFlags(&up[s], cudaEventDisableTiming));
     }
+    if (rc == KS_OK) rc = cuda_status(cudaStreamCreateWithFlags(&sdw, cudaStreamNonBlocking));
     if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dxin, tbytes, st[0]));
     if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dgy, tbytes, st[0]));
     if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dkk, sizeof(float) * H * K, st[0]));
@@ -193,18 +206,22 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
         const size_t off = size_t(b0) * H * L, bytes = entry * bn;
         rc = cuda_status(cudaMemcpyAsync(dxin + off, x + off, bytes, cudaMemcpyHostToDevice, st[s]));
         if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dgy + off, gy + off, bytes, cudaMemcpyHostToDevice, st[s]));
+        if (rc == KS_OK) rc = cuda_status(cudaEventRecord(up[s], st[s]));
         if (rc == KS_OK) rc = ks_dwconv1d_fwd_f32(dxin + off, dkk, dy[s], bn, H, L, K, mode, st[s]);
         if (rc == KS_OK) rc = ks_dwconv1d_dx_f32(dgy + off, dkk, ddx[s], bn, H, L, K, mode, st[s]);
         if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(y + off, dy[s], bytes, cudaMemcpyDeviceToHost, st[s]));
         if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dxo + off, ddx[s], bytes, cudaMemcpyDeviceToHost, st[s]));
     }
-    // dW after every upload: stream 0 waits for the other streams
-    for (int s = 1; s < slots && rc == KS_OK; ++s) {
-        rc = cuda_status(cudaEventRecord(ev[s], st[s]));
-        if (rc == KS_OK) rc = cuda_status(cudaStreamWaitEvent(st[0], ev[s], 0));
+    // dW once every upload has landed (not after the downloads): its own
+    // stream waits on each slot stream's last upload, so dW and dk's copy
+    // overlap the trailing y / dx downloads
+    for (int s = 0; s < slots && rc == KS_OK; ++s) rc = cuda_status(cudaStreamWaitEvent(sdw, up[s], 0));
+    if (rc == KS_OK) rc = ks_dwconv1d_dw_f32(dgy, dxin, ddk, B, H, L, K, scheme, chunk, mode, nullptr, 0, sdw);
+    if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dk, ddk, sizeof(float) * H * K, cudaMemcpyDeviceToHost, sdw));
+    if (sdw) {
+        const ks_status e = cuda_status(cudaStreamSynchronize(sdw));
+        if (rc == KS_OK) rc = e;
     }
-    if (rc == KS_OK) rc = ks_dwconv1d_dw_f32(dgy, dxin, ddk, B, H, L, K, scheme, chunk, mode, nullptr, 0, st[0]);
-    if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dk, ddk, sizeof(float) * H * K, cudaMemcpyDeviceToHost, st[0]));
     for (int s = 0; s < slots; ++s)
         if (st[s]) cudaStreamSynchronize(st[s]);
     if (st[0]) {
@@ -222,7 +239,9 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
     for (int s = 0; s < slots; ++s) {
         if (st[s]) cudaStreamDestroy(st[s]);
         if (ev[s]) cudaEventDestroy(ev[s]);
+        if (up[s]) cudaEventDestroy(up[s]);
     }
+    if (sdw) cudaStreamDestroy(sdw);
     return rc;
 }
 
