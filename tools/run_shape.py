@@ -16,6 +16,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("shape", type=int, nargs=4)
 ap.add_argument("--reps", type=int, default=2)
 ap.add_argument("--scheme", default="hierarchical")
+ap.add_argument("--bwd", action="store_true", help="also run the fused backward (ks_dwconv1d_bwd_f32)")
 a = ap.parse_args()
 B, H, L, K = a.shape
 scheme = {"hierarchical": ks.HIERARCHICAL, "pairwise": ks.PAIRWISE}[a.scheme]
@@ -24,5 +25,7 @@ for _ in range(a.reps):
     y = ks.forward(x, k, ks.FUSED)
     dx = ks.backward_input(gy, k, ks.FUSED)
     dk = ks.backward_weight(gy, x, K, scheme, 0, ks.FUSED)
+    if a.bwd:
+        dx2, dk2 = ks.backward(gy, x, k, ks.FUSED)
 torch.cuda.synchronize()
 print("done", float(y.abs().sum()), float(dx.abs().sum()), float(dk.abs().sum()))
