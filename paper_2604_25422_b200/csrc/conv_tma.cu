@@ -73,6 +73,27 @@ bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64
     return r == CUDA_SUCCESS;
 }
 
+// Padded row view: the [rows, L] tensor as {32, L/32, rows} with box
+// {36, n, 1} -- the box's inner extent runs 4 floats past the inner dimension,
+// so every 128-byte global piece lands as a 144-byte shared row (the excess
+// quad is out of bounds and never fetched).  Same padded layout as
+// encode_padded_view, but TMA moves 128-byte rows instead of 16-byte ones:
+// 7.07 TB/s streamed vs 4.05 for the 5-D view (tools/probes/tma_box_probe.cu
+// on the B200; 7.25 for the 128B-swizzled 32-float box).
+bool encode_row_view_padded(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int n) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || L % 32 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+    if (rows >= (int64_t(1) << 31) || L / 32 >= (int64_t(1) << 31) || n < 1 || n > 256) return false;
+    const cuuint64_t dims[3] = {32, static_cast<cuuint64_t>(L / 32), static_cast<cuuint64_t>(rows)};
+    const cuuint64_t strides[2] = {128, static_cast<cuuint64_t>(L) * 4};
+    const cuuint32_t box[3] = {36, static_cast<cuuint32_t>(n), 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // kp[h, 0:Kp) = `lead` zeros, then k[h, j] (forward) or k[h, K-1-j] (dX, the
 // reference's k[h, K-1-j] of src/conv_core.cpp:68), zero padded to Kp.
 __global__ void prep_taps(const float* __restrict__ k, float* __restrict__ kp, int64_t H, int64_t K, int64_t Kp,

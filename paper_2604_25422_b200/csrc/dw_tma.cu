@@ -337,11 +337,29 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
 
 }  // namespace
 
+ks_status bwd_short_dw_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
+                              cudaStream_t, bool*);
+ks_status bwd_short_fused_stage1(const float*, const float*, const float*, float*, float*, int64_t, int64_t,
+                                 int64_t, int64_t, int, int, cudaStream_t, bool*);
+
+// K <= 16: the K-specialised kernels of bwd_short.cuh (same bits, fewer
+// instructions) unless an A/B knob asks for this file's generic kernel.
+static bool use_bwd_short(int64_t K) {
+    if (K > 16) return false;
+    const char* e = getenv("KS_BWDS");
+    if (e && *e == '0') return false;
+    return !getenv("KS_DWTMA_NS") && !(getenv("KS_DWTMA_J16") && *getenv("KS_DWTMA_J16") == '0');
+}
+
 // Stage 1 of HIERARCHICAL dW through TMA into part[G,H,K] (G = the caller's row
 // groups; stage 2 is shared with the generic path).  *handled = false means
 // the shape is not supported here and the caller falls back.
 ks_status dw_tma_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
                         int G, int mode, cudaStream_t st, bool* handled) {
+    if (use_bwd_short(K)) {
+        const ks_status s = bwd_short_dw_stage1(gy, x, part, B, H, L, K, G, mode, st, handled);
+        if (*handled) return s;
+    }
     return run_dw_tma(gy, x, nullptr, nullptr, part, B, H, L, K, G, mode, false, st, handled);
 }
 
@@ -352,6 +370,10 @@ ks_status bwd_tma_stage1(const float* gy, const float* x, const float* k, float*
     if (K > 16 || (reinterpret_cast<uintptr_t>(dx) & 15) != 0) {
         *handled = false;
         return KS_OK;
+    }
+    if (use_bwd_short(K)) {
+        const ks_status s = bwd_short_fused_stage1(gy, x, k, dx, part, B, H, L, K, G, mode, st, handled);
+        if (*handled) return s;
     }
     return run_dw_tma(gy, x, k, dx, part, B, H, L, K, G, mode, true, st, handled);
 }

@@ -177,4 +177,8 @@ bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t 
 bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
                         int chan_box, int depth);
 
+// Host: the {32, L/32, rows} view with box {36, n, 1}: the same 36-float padded
+// shared rows from 128-byte global rows (streams at near copy bandwidth).
+bool encode_row_view_padded(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int n);
+
 }  // namespace ks

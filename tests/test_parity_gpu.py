@@ -298,6 +298,27 @@ def test_fused_backward_equals_separate_calls(shape):
         assert same(host(dk), host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))), m
 
 
+@pytest.mark.parametrize("K", list(range(1, 17)))
+def test_bwd_short_equals_generic_kernels(K, monkeypatch):
+    """The K-specialised short-kernel dW and fused backward (bwd_short.cuh)
+    against the generic dw_tma kernels they replace (KS_BWDS=0): dk and dx
+    bit for bit, every K in 1..16, both multiply-add modes, a ragged last
+    tile (L = 4160) and several work items per CTA."""
+    B, H, L = 6, 3, 4160
+    x, k, gy = ks.make_inputs(11, B, H, L, K)
+    for m in (SEPARATE, FUSED):
+        monkeypatch.setenv("KS_BWDS", "0")
+        dk_g = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
+        dx_g, dk2_g = (host(t) for t in ks.backward(gy, x, k, m))
+        monkeypatch.delenv("KS_BWDS")
+        dk_s = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
+        dx_s, dk2_s = (host(t) for t in ks.backward(gy, x, k, m))
+        assert same(dk_s, dk_g), m
+        assert same(dk2_s, dk2_g), m
+        assert same(dx_s, dx_g), m
+        assert same(dx_s, host(ks.backward_input(gy, k, m))), m
+
+
 def test_fused_backward_config3_against_oracle(oracle):
     """At config 3 (4 GiB per tensor): the fused backward's dx on sampled
     channels bitwise against the oracle, dk to tolerance against fp64."""
