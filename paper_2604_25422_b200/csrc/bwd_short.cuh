@@ -1,27 +1,30 @@
-// bwd_short.cuh -- short-kernel (K <= 16) weight gradient and fused backward,
-// fully specialised on K (sm_100a).  Included by bwd_short_dw.cu (dW only) and
-// bwd_short_dx.cu (dX + dW in one pass).
+// bwd_short.cuh -- the short-kernel (K <= 16) paths, fully specialised on K
+// (sm_100a): HIERARCHICAL dW stage 1, the fused backward (dX + dW in one pass),
+// and the forward / dX stencils.  Instantiated by bwd_short_{dw,dx,st}.cu.
 //
-//   dk[h,j] = sum_b sum_t gy[b,h,t] * x[b,h,t+j-p]    (reference src/conv_core.cpp:148-181)
-//   dx[b,h,t] = sum_j gy[b,h,t+j-q] * k[h,K-1-j]       (reference src/conv_core.cpp:48-75)
+//   y[b,h,t]  = sum_j x[b,h,t+j-p] * k[h,j]             (reference src/conv_core.cpp:21-46)
+//   dx[b,h,t] = sum_j gy[b,h,t+j-q] * k[h,K-1-j]        (src/conv_core.cpp:48-75)
+//   dk[h,j]   = sum_b sum_t gy[b,h,t] * x[b,h,t+j-p]    (src/conv_core.cpp:148-181)
 //
-// Same decomposition and association order as dw_tma (dw_tma.cu) -- CTA =
-// (row group, channel), 256 threads, work items = (row, 2048-wide t tile) in
-// flat order, thread (warp w, lane l) owns the 8-wide t block at
-// tl = 32 l + 8 (w & 3) + 1024 (w >> 2), ascending-t FMA chains per tap, the
-// same xor-shuffle / warp tree -- so dk is bit-identical to the dW-only call
-// and dx to the stencil.  What changes is the instruction stream around the
-// FMAs, which ncu showed was half of the issued instructions at K = 16
-// (the fused backward at config 5a was issue-bound at 82% of slots):
+// Work items are (row, 2048-wide t tile); 256 threads, thread (warp w, lane l)
+// owns the 8-wide t block at tl = 32 l + 8 (w & 3) + 1024 (w >> 2).  For dW
+// this is dw_tma's decomposition (dw_tma.cu): CTA = (row group, channel),
+// items in flat order, ascending-t FMA chains per tap, the same xor-shuffle /
+// warp tree -- so dk is bit-identical to dw_tma's.  Every output of the
+// stencils is the reference's ascending-j chain from +0 (zero-filled halo taps
+// add +-0, which never changes a chain that starts at +0), so y and dx are
+// bit-identical to the reference.  What this file changes is the instruction
+// stream around the FMAs (half of all issued instructions at K = 16 in
+// dw_tma, where the fused backward at config 5a was issue-bound at 82%):
 //
 // * K, p, q and every window offset are template constants: no tap-count
 //   branches, no runtime sub-quad offsets.
-// * gy and x land through the padded row view (encode_row_view_padded: box
-//   {36, n} over 32-float pieces, 128-byte global rows): every 32-float piece
-//   is a 36-float shared row, so a thread's quads sit at
-//   (piece * 144 + compile-time) bytes and every LDS.128 is [base + imm] --
-//   conflict-free (lanes 144 B apart) with no swizzle arithmetic.  The column
-//   8 (w & 3) is made compile-time by one warp-uniform switch at entry.
+// * Tiles land through the padded row view (encode_row_view_padded: box
+//   {36, n} over 32-float pieces, 128-byte global rows): every piece is a
+//   36-float shared row, so a thread's quads sit at (piece * 144 +
+//   compile-time) bytes and every LDS.128 is [base + imm] -- conflict-free
+//   (lanes 144 B apart) with no swizzle arithmetic.  The column 8 (w & 3) is
+//   made compile-time by one warp-uniform switch at entry.
 // * The fused kernel takes the 8 gy values of the dW block from the dX
 //   window it already holds (the dX window of a block covers gy[t, t+8)).
 // * Stage / phase / (row, tile) are carried incrementally: no integer
@@ -34,95 +37,128 @@
 namespace ks {
 namespace bwds {
 
+// MODE: what a kernel instance computes
+constexpr int kDW = 0;      // HIERARCHICAL dW stage 1 (part[G,H,K])
+constexpr int kFUSED = 1;   // dX + dW stage 1 from one pass over gy and x
+constexpr int kFWD = 2;     // forward stencil: out = x (*) k, offset p
+constexpr int kDXS = 3;     // dX stencil: out = gy (*) reversed k, offset q
+
 constexpr int kThreads = 256;
 constexpr int kTT = 2048;                // t per work item
 constexpr int kPitch = 144;              // bytes per padded 32-float piece
-constexpr int kXP = 66;                  // x window pieces (2048 + taps + register overrun)
+constexpr int kXP = 66;                  // window pieces (2048 + halo / taps + register overrun)
 constexpr int kXRegion = (kXP * kPitch + 127) / 128 * 128;  // 9600
-constexpr int kOutBytes = kTT * 4;       // one dX tile, 128B-swizzled rows
+constexpr int kOutBytes = kTT * 4;       // one output tile, 128B-swizzled rows
 
-template <int KT, bool DX>
+template <int KT, int MODE>
 struct Geo {
+    static constexpr bool HAS_DW = MODE <= kFUSED;  // x window + dW accumulators
+    static constexpr bool HAS_ST = MODE >= kFUSED;  // a stencil output tile per item
     static constexpr int p = KT / 2;
     static constexpr int q = KT - 1 - p;                  // dX offset (src/conv_core.cpp:56)
     static constexpr int D = (32 - p % 32) % 32;          // x window origin t0 - p - D on a piece
     static constexpr int A = D & ~3;
     static constexpr int S = D & 3;                       // (-p) mod 4
     static constexpr int XR0 = (p + D) / 32;              // x window first piece = t0/32 - XR0
-    static constexpr int S2 = (4 - q % 4) % 4;            // (-q) mod 4
-    static constexpr int QS = q + S2;                     // multiple of 4
+    static constexpr int OFF = MODE == kFWD ? p : q;      // stencil offset
+    static constexpr int S2 = (4 - OFF % 4) % 4;          // (-OFF) mod 4
+    static constexpr int QS = OFF + S2;                   // multiple of 4
     static constexpr int NVX = (S + 8 + KT - 1 + 3) / 4;  // x quads per block
-    static constexpr int NV2 = (S2 + 8 + KT - 1 + 3) / 4; // dX window quads per block
-    static constexpr int GYP = DX ? 66 : 64;              // gy pieces (DX: one halo piece each side)
+    static constexpr int NV2 = (S2 + 8 + KT - 1 + 3) / 4; // stencil window quads per block
+    static constexpr int GYP = MODE == kDW ? 64 : 66;     // stencil input: one halo piece each side
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
-    static constexpr int Stage = GYRegion + kXRegion;
-    static constexpr int NS = KT <= 8 ? 4 : 3;            // as dw_tma: 4 stages when the FMAs are light
-    static constexpr uint32_t TX = static_cast<uint32_t>((GYP + kXP) * kPitch);
-    static constexpr int Smem = (DX ? 2 * kOutBytes : 0) + NS * Stage + 64 + 1024;
+    static constexpr int TapBytes = MODE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
+    static constexpr int Stage = GYRegion + (HAS_DW ? kXRegion : 0) + TapBytes;
+    static constexpr int NS = MODE >= kFWD ? 4 : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
+    static constexpr int MinBlocks = MODE >= kFWD ? 4 : 3;
+    static constexpr uint32_t TX =
+        static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (MODE >= kFWD ? 64 : 0));
+    static constexpr int Smem = (HAS_ST ? 2 * kOutBytes : 0) + NS * Stage + 64 + 1024;
     static_assert(QS % 4 == 0 && QS + 8 <= 4 * NV2, "gy block inside the dX window");
     static_assert(A + 2040 + 4 * NVX <= kXP * 32, "x window inside the staged pieces");
+    static_assert(!HAS_ST || 32 + 2040 - QS + 4 * NV2 <= GYP * 32, "stencil window inside the staged pieces");
 };
 
 // byte offset of the quad at logical index e (>= 0, 4-aligned) from a piece base
 __host__ __device__ constexpr int pofs(int e) { return (e >> 5) * kPitch + (e & 31) * 4; }
 
-template <int KT, bool FUSED, bool DX, int C0>
-__device__ __forceinline__ void run(const CUtensorMap* gy_map, const CUtensorMap* x_map, const CUtensorMap* dx_map,
+struct Args {
+    int H, L;
+    int row0, rstep, nrows;  // this CTA's rows: row0 + i * rstep, i < nrows (row = b * H + h)
+    int h;                   // dW modes: the CTA's channel
+    int grp;                 // dW modes: the CTA's row group
+};
+
+template <int KT, bool FUSED, int MODE, int C0>
+__device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap* x_map, const CUtensorMap* out_map,
                                     const float* __restrict__ k, float* __restrict__ part, unsigned char* smem,
-                                    uint64_t* full, float (*red)[KT], int H, int L, int h, int grp, int b_begin,
-                                    int b_end) {
-    using Gm = Geo<KT, DX>;
+                                    uint64_t* full, float (*red)[KT], const Args a) {
+    using Gm = Geo<KT, MODE>;
     constexpr int NS = Gm::NS;
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
-    const int ntt = (L + kTT - 1) / kTT;
-    const int nunits = (b_end - b_begin) * ntt;
-    unsigned char* stages = smem + (DX ? 2 * kOutBytes : 0);
+    const int ntt = (a.L + kTT - 1) / kTT;
+    const int nunits = a.nrows * ntt;
+    unsigned char* stages = smem + (Gm::HAS_ST ? 2 * kOutBytes : 0);
 
     // producer state (thread 0): next item to load
-    int ib = b_begin, it0 = 0;
+    int irow = a.row0, it0 = 0;
     auto issue = [&](int stage) {
         uint64_t* bar = &full[stage];
+        unsigned char* sb = stages + stage * Gm::Stage;
         mbar_arrive_expect_tx(bar, Gm::TX);
-        const int row = ib * H + h;
-        tma_load_3d(stages + stage * Gm::Stage, gy_map, 0, it0 / 32 - (DX ? 1 : 0), row, bar);
-        tma_load_3d(stages + stage * Gm::Stage + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, row, bar);
+        tma_load_3d(sb, in_map, 0, it0 / 32 - (MODE == kDW ? 0 : 1), irow, bar);
+        if constexpr (Gm::HAS_DW) tma_load_3d(sb + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, irow, bar);
+        if constexpr (MODE >= kFWD) bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * 16, 64, bar);
         it0 += kTT;
-        if (it0 >= L) {
+        if (it0 >= a.L) {
             it0 = 0;
-            ++ib;
+            irow += a.rstep;
         }
     };
     if (tid == 0)
         for (int s = 0; s < NS && s < nunits; ++s) issue(s);
 
-    float wr[DX ? KT : 1];
-    if constexpr (DX) {
+    // stencil taps: the fused backward holds the CTA's reversed row in
+    // registers; the stencils read the row's prepared taps (prep_taps:
+    // reversed for dX, zero past K) from each stage
+    float w[Gm::HAS_ST ? 16 : 1];
+    if constexpr (MODE == kFUSED) {
 #pragma unroll
-        for (int jj = 0; jj < KT; ++jj) wr[jj] = k[static_cast<int64_t>(h) * KT + KT - 1 - jj];
+        for (int jj = 0; jj < KT; ++jj) w[jj] = k[static_cast<int64_t>(a.h) * KT + KT - 1 - jj];
     }
-    float acc[KT];
+    float acc[Gm::HAS_DW ? KT : 1];
 #pragma unroll
-    for (int i = 0; i < KT; ++i) acc[i] = 0.f;
+    for (int i = 0; i < (Gm::HAS_DW ? KT : 1); ++i) acc[i] = 0.f;
 
     const int R = lane + 32 * (warp >> 2);  // piece of this thread's block within the tile
     const unsigned char* tb = stages + R * kPitch;
-    // dX tile: 128B-swizzled rows of 32 floats, this thread's 8 outputs at row R, quads C0/4, C0/4+1
+    // output tile: 128B-swizzled rows of 32 floats, this thread's 8 outputs at row R, quads C0/4, C0/4+1
     const uint32_t o0 = static_cast<uint32_t>(R * 128 + (((C0 / 4) ^ (R & 7)) << 4));
     const uint32_t o1 = static_cast<uint32_t>(R * 128 + (((C0 / 4 + 1) ^ (R & 7)) << 4));
 
-    int stage = 0, t0 = 0, b = b_begin;
+    int stage = 0, t0 = 0, row = a.row0;
     uint32_t phase = 0;
     for (int u = 0; u < nunits; ++u) {
         mbar_wait(&full[stage], phase);
         const unsigned char* gys = tb + stage * Gm::Stage;
-        const unsigned char* xs = gys + Gm::GYRegion;
         unsigned char* ob = smem + (u & 1) * kOutBytes;
-        if (t0 + 32 * R < L) {
+        if constexpr (MODE >= kFWD) {
+            const float* tp = reinterpret_cast<const float*>(stages + stage * Gm::Stage + Gm::GYRegion);
+#pragma unroll
+            for (int c = 0; c < (KT + 3) / 4; ++c) {
+                const float4 qv = *reinterpret_cast<const float4*>(tp + 4 * c);
+                w[4 * c + 0] = qv.x;
+                w[4 * c + 1] = qv.y;
+                w[4 * c + 2] = qv.z;
+                w[4 * c + 3] = qv.w;
+            }
+        }
+        if (t0 + 32 * R < a.L) {
             float gv[8];
-            if constexpr (DX) {
-                // dx[t0+tl+r] = sum_j gy[t0+tl+r+j-q] * k[K-1-j], j ascending from +0;
-                // window quad c = gy logical (t0-32 origin) 32 + tl - QS + 4c
+            if constexpr (Gm::HAS_ST) {
+                // out[t0+tl+r] = sum_j in[t0+tl+r+j-OFF] * w[j], j ascending from +0;
+                // window quad c = input logical (t0-32 origin) 32 + tl - QS + 4c
                 float v2[4 * Gm::NV2];
 #pragma unroll
                 for (int c = 0; c < Gm::NV2; ++c) {
@@ -138,11 +174,13 @@ __device__ __forceinline__ void run(const CUtensorMap* gy_map, const CUtensorMap
 #pragma unroll
                 for (int jj = 0; jj < KT; ++jj)
 #pragma unroll
-                    for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v2[Gm::S2 + r + jj], wr[jj]);
+                    for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v2[Gm::S2 + r + jj], w[jj]);
                 *reinterpret_cast<float4*>(ob + o0) = make_float4(d[0], d[1], d[2], d[3]);
                 *reinterpret_cast<float4*>(ob + o1) = make_float4(d[4], d[5], d[6], d[7]);
+                if constexpr (MODE == kFUSED) {
 #pragma unroll
-                for (int tt = 0; tt < 8; ++tt) gv[tt] = v2[Gm::QS + tt];
+                    for (int tt = 0; tt < 8; ++tt) gv[tt] = v2[Gm::QS + tt];
+                }
             } else {
 #pragma unroll
                 for (int c = 0; c < 2; ++c) {
@@ -153,29 +191,32 @@ __device__ __forceinline__ void run(const CUtensorMap* gy_map, const CUtensorMap
                     gv[4 * c + 3] = qv.w;
                 }
             }
-            // dW: x logical (origin t0 - p - D) A + tl + 4c; acc[jj] += gy[t] * x[t + jj - p]
-            float xv[4 * Gm::NVX];
+            if constexpr (Gm::HAS_DW) {
+                // dW: x logical (origin t0 - p - D) A + tl + 4c; acc[jj] += gy[t] * x[t + jj - p]
+                const unsigned char* xs = gys + Gm::GYRegion;
+                float xv[4 * Gm::NVX];
 #pragma unroll
-            for (int c = 0; c < Gm::NVX; ++c) {
-                const float4 qv = lds4(xs + pofs(Gm::A + C0 + 4 * c));
-                xv[4 * c + 0] = qv.x;
-                xv[4 * c + 1] = qv.y;
-                xv[4 * c + 2] = qv.z;
-                xv[4 * c + 3] = qv.w;
+                for (int c = 0; c < Gm::NVX; ++c) {
+                    const float4 qv = lds4(xs + pofs(Gm::A + C0 + 4 * c));
+                    xv[4 * c + 0] = qv.x;
+                    xv[4 * c + 1] = qv.y;
+                    xv[4 * c + 2] = qv.z;
+                    xv[4 * c + 3] = qv.w;
+                }
+#pragma unroll
+                for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+                    for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
             }
-#pragma unroll
-            for (int tt = 0; tt < 8; ++tt)
-#pragma unroll
-                for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
         }
-        if constexpr (DX) {
-            fence_proxy_async_smem();           // dX tile visible to the TMA store
+        if constexpr (Gm::HAS_ST) {
+            fence_proxy_async_smem();           // output tile visible to the TMA store
             if (tid == 0) bulk_wait_read_all();  // store u-1 has read buffer (u+1)&1
         }
         __syncthreads();
         if (tid == 0) {
-            if constexpr (DX) {
-                tma_store_3d(dx_map, ob, 0, t0 / 32, b * H + h);  // columns past L are clipped
+            if constexpr (Gm::HAS_ST) {
+                tma_store_3d(out_map, ob, 0, t0 / 32, row);  // columns past L are clipped
                 bulk_commit();
             }
             if (u + NS < nunits) issue(stage);
@@ -185,69 +226,84 @@ __device__ __forceinline__ void run(const CUtensorMap* gy_map, const CUtensorMap
             phase ^= 1u;
         }
         t0 += kTT;
-        if (t0 >= L) {
+        if (t0 >= a.L) {
             t0 = 0;
-            ++b;
+            row += a.rstep;
         }
     }
-    if (DX && tid == 0) bulk_wait_all();
+    if (Gm::HAS_ST && tid == 0) bulk_wait_all();
 
-    // fixed xor-shuffle tree per warp, then the 8 warps in ascending order (as dw_tma)
+    if constexpr (Gm::HAS_DW) {
+        // fixed xor-shuffle tree per warp, then the 8 warps in ascending order (as dw_tma)
 #pragma unroll
-    for (int jj = 0; jj < KT; ++jj) {
-        float v = acc[jj];
+        for (int jj = 0; jj < KT; ++jj) {
+            float v = acc[jj];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        acc[jj] = v;
-    }
-    if (lane == 0) {
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            acc[jj] = v;
+        }
+        if (lane == 0) {
 #pragma unroll
-        for (int jj = 0; jj < KT; ++jj) red[warp][jj] = acc[jj];
-    }
-    __syncthreads();
-    if (tid < KT) {
-        float s = 0.f;
+            for (int jj = 0; jj < KT; ++jj) red[warp][jj] = acc[jj];
+        }
+        __syncthreads();
+        if (tid < KT) {
+            float s = 0.f;
 #pragma unroll
-        for (int w = 0; w < kThreads / 32; ++w) s += red[w][tid];
-        part[(static_cast<int64_t>(grp) * H + h) * KT + tid] = s;
+            for (int ww = 0; ww < kThreads / 32; ++ww) s += red[ww][tid];
+            part[(static_cast<int64_t>(a.grp) * a.H + a.h) * KT + tid] = s;
+        }
     }
 }
 
-template <int KT, bool FUSED, bool DX>
-__global__ void __launch_bounds__(kThreads, 3)  // 3 CTAs per SM: <= 80 registers
-bwd_short(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUtensorMap x_map,
-          const __grid_constant__ CUtensorMap dx_map, const float* __restrict__ k, float* __restrict__ part, int B,
+// dW modes: grid = G x H CTAs, CTA = (row group, channel).  Stencils: a
+// persistent grid, CTA c takes rows c, c + gridDim.x, ...
+template <int KT, bool FUSED, int MODE>
+__global__ void __launch_bounds__(kThreads, Geo<KT, MODE>::MinBlocks)  // 3 CTAs/SM (<= 80 regs), stencils 4
+bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap x_map,
+          const __grid_constant__ CUtensorMap out_map, const float* __restrict__ k, float* __restrict__ part, int B,
           int H, int L, int G) {
-    using Gm = Geo<KT, DX>;
+    using Gm = Geo<KT, MODE>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (DX ? 2 * kOutBytes : 0) + Gm::NS * Gm::Stage);
-    __shared__ float red[kThreads / 32][KT];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (Gm::HAS_ST ? 2 * kOutBytes : 0) + Gm::NS * Gm::Stage);
+    __shared__ float red[Gm::HAS_DW ? kThreads / 32 : 1][KT];
 
-    const int h = blockIdx.x % H;
-    const int grp = blockIdx.x / H;
-    const int b_begin = static_cast<int>(static_cast<int64_t>(B) * grp / G);
-    const int b_end = static_cast<int>(static_cast<int64_t>(B) * (grp + 1) / G);
+    Args a;
+    a.H = H;
+    a.L = L;
+    if constexpr (Gm::HAS_DW) {
+        a.h = blockIdx.x % H;
+        a.grp = blockIdx.x / H;
+        const int b_begin = static_cast<int>(static_cast<int64_t>(B) * a.grp / G);
+        const int b_end = static_cast<int>(static_cast<int64_t>(B) * (a.grp + 1) / G);
+        a.row0 = b_begin * H + a.h;
+        a.rstep = H;
+        a.nrows = b_end - b_begin;
+    } else {
+        const int rows = B * H;
+        a.h = a.grp = 0;
+        a.row0 = blockIdx.x;
+        a.rstep = gridDim.x;
+        a.nrows = static_cast<int>(blockIdx.x) < rows
+                      ? (rows - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                      : 0;
+    }
     if (threadIdx.x == 0) {
-        prefetch_tmap(&gy_map);
-        prefetch_tmap(&x_map);
-        if (DX) prefetch_tmap(&dx_map);
+        prefetch_tmap(&in_map);
+        if (Gm::HAS_DW) prefetch_tmap(&x_map);
+        if (Gm::HAS_ST) prefetch_tmap(&out_map);
         for (int s = 0; s < Gm::NS; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
     }
     __syncthreads();
     switch ((threadIdx.x >> 5) & 3) {  // warp-uniform: the block's column 8 (w & 3) becomes a constant
-        case 0: run<KT, FUSED, DX, 0>(&gy_map, &x_map, &dx_map, k, part, smem, full, red, H, L, h, grp, b_begin, b_end); break;
-        case 1: run<KT, FUSED, DX, 8>(&gy_map, &x_map, &dx_map, k, part, smem, full, red, H, L, h, grp, b_begin, b_end); break;
-        case 2: run<KT, FUSED, DX, 16>(&gy_map, &x_map, &dx_map, k, part, smem, full, red, H, L, h, grp, b_begin, b_end); break;
-        default: run<KT, FUSED, DX, 24>(&gy_map, &x_map, &dx_map, k, part, smem, full, red, H, L, h, grp, b_begin, b_end); break;
+        case 0: run<KT, FUSED, MODE, 0>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
+        case 1: run<KT, FUSED, MODE, 8>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
+        case 2: run<KT, FUSED, MODE, 16>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
+        default: run<KT, FUSED, MODE, 24>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
     }
 }
-
-// Host launcher for one K: maps, smem opt-in, launch.
-template <bool DX>
-ks_status launch_bwd_short(const float* gy, const float* x, const float* k, float* dx, float* part, int64_t B,
-                           int64_t H, int64_t L, int64_t K, int G, int mode, cudaStream_t st);
 
 }  // namespace bwds
 }  // namespace ks

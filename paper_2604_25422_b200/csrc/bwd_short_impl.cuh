@@ -1,42 +1,64 @@
-// bwd_short_impl.cuh -- host launcher of bwd_short (bwd_short.cuh) for one of
-// the two kernel families; instantiated by bwd_short_dw.cu / bwd_short_dx.cu so
-// the 2 x 16 x 2 specialisations compile in parallel.
+// bwd_short_impl.cuh -- host launchers of bwd_short (bwd_short.cuh) for one
+// kernel family; included by bwd_short_dw.cu / bwd_short_dx.cu /
+// bwd_short_st.cu so the specialisations compile in parallel.
 #pragma once
+
+#include <algorithm>
 
 #include "bwd_short.cuh"
 
 namespace ks {
 
+__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
+
 namespace bwds {
 
-template <int KT, bool FUSED, bool DX>
-ks_status launch_k(const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& dm, const float* k, float* part,
+template <int KT, bool FUSED, int MODE>
+ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k, float* part,
                    int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
-    auto kern = bwd_short<KT, FUSED, DX>;
-    constexpr int smem = Geo<KT, DX>::Smem;
-    prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
-    const unsigned blocks = static_cast<unsigned>(int64_t(G) * H);
-    kern<<<blocks, kThreads, smem, st>>>(gm, xm, dm, k, part, static_cast<int>(B), static_cast<int>(H),
-                                         static_cast<int>(L), G);
+    auto kern = bwd_short<KT, FUSED, MODE>;
+    constexpr int smem = Geo<KT, MODE>::Smem;
+    const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
+    const int64_t blocks = MODE <= kFUSED ? int64_t(G) * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
+    kern<<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(im, xm, om, k, part, static_cast<int>(B),
+                                                                static_cast<int>(H), static_cast<int>(L), G);
     return check_launch();
 }
 
-template <int KT, bool DX>
-ks_status launch_m(bool fused, const CUtensorMap& gm, const CUtensorMap& xm, const CUtensorMap& dm, const float* k,
+template <int KT, int MODE>
+ks_status launch_m(bool fused, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k,
                    float* part, int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
-    return fused ? launch_k<KT, true, DX>(gm, xm, dm, k, part, B, H, L, G, st)
-                 : launch_k<KT, false, DX>(gm, xm, dm, k, part, B, H, L, G, st);
+    return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, st)
+                 : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, st);
 }
 
+template <int MODE>
+ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om,
+                       const float* k, float* part, int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
+    switch (K) {
+#define KS_BWDS_CASE(KV) \
+    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, st);
+        KS_BWDS_CASE(1) KS_BWDS_CASE(2) KS_BWDS_CASE(3) KS_BWDS_CASE(4) KS_BWDS_CASE(5) KS_BWDS_CASE(6)
+        KS_BWDS_CASE(7) KS_BWDS_CASE(8) KS_BWDS_CASE(9) KS_BWDS_CASE(10) KS_BWDS_CASE(11) KS_BWDS_CASE(12)
+        KS_BWDS_CASE(13) KS_BWDS_CASE(14) KS_BWDS_CASE(15) KS_BWDS_CASE(16)
+#undef KS_BWDS_CASE
+        default: return KS_ERR_CUDA;
+    }
+}
+
+inline bool shape_ok(int64_t B, int64_t H, int64_t L, int64_t K) {
+    return K >= 1 && K <= 16 && L % 32 == 0 && B * H < (int64_t(1) << 31) && L < (int64_t(1) << 30);
+}
+
+// dW (DX = false) or the fused backward (DX = true).  *handled = false: shape
+// or alignment outside the envelope (the caller falls back to dw_tma).
 template <bool DX>
 ks_status launch_bwd_short(const float* gy, const float* x, const float* k, float* dx, float* part, int64_t B,
                            int64_t H, int64_t L, int64_t K, int G, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
-    if (K < 1 || K > 16 || L % 32 != 0 || B * H >= (int64_t(1) << 31) || L >= (int64_t(1) << 30) ||
-        int64_t(G) * H >= (int64_t(1) << 31))
-        return KS_OK;
+    if (!shape_ok(B, H, L, K) || int64_t(G) * H >= (int64_t(1) << 31)) return KS_OK;
     CUtensorMap gm, xm, dm;
-    if (!encode_row_view_padded(&gm, gy, B * H, L, Geo<1, DX>::GYP)) return KS_OK;
+    if (!encode_row_view_padded(&gm, gy, B * H, L, DX ? 66 : 64)) return KS_OK;
     if (!encode_row_view_padded(&xm, x, B * H, L, kXP)) return KS_OK;
     if constexpr (DX) {
         if (!encode_row_view(&dm, dx, B * H, L, 32, kTT / 32, 128)) return KS_OK;
@@ -45,15 +67,33 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
     }
     *handled = true;
     const bool f = mode == KS_MULADD_FUSED;
-    switch (K) {
-#define KS_BWDS_CASE(KV) \
-    case KV: return launch_m<KV, DX>(f, gm, xm, dm, k, part, B, H, L, G, st);
-        KS_BWDS_CASE(1) KS_BWDS_CASE(2) KS_BWDS_CASE(3) KS_BWDS_CASE(4) KS_BWDS_CASE(5) KS_BWDS_CASE(6)
-        KS_BWDS_CASE(7) KS_BWDS_CASE(8) KS_BWDS_CASE(9) KS_BWDS_CASE(10) KS_BWDS_CASE(11) KS_BWDS_CASE(12)
-        KS_BWDS_CASE(13) KS_BWDS_CASE(14) KS_BWDS_CASE(15) KS_BWDS_CASE(16)
-#undef KS_BWDS_CASE
-        default: return KS_ERR_CUDA;
+    return DX ? launch_any_k<kFUSED>(K, f, gm, xm, dm, k, part, B, H, L, G, st)
+              : launch_any_k<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, st);
+}
+
+// Forward (reverse = 0, off = p) or dX (reverse = 1, off = q) stencil.
+inline ks_status launch_stencil_short(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L,
+                                      int64_t K, int64_t off, int reverse, int mode, cudaStream_t st,
+                                      bool* handled) {
+    *handled = false;
+    if (!shape_ok(B, H, L, K) || off != (reverse ? K - 1 - K / 2 : K / 2)) return KS_OK;
+    CUtensorMap im, om;
+    if (!encode_row_view_padded(&im, in, B * H, L, 66)) return KS_OK;
+    if (!encode_row_view(&om, out, B * H, L, 32, kTT / 32, 128)) return KS_OK;
+    float* kp = nullptr;
+    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * 16, st));
+    if (rc != KS_OK) return rc;
+    *handled = true;
+    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st>>>(k, kp, H, K, 16,
+                                                                                                   reverse, 0);
+    rc = check_launch();
+    if (rc == KS_OK) {
+        const bool f = mode == KS_MULADD_FUSED;
+        rc = reverse ? launch_any_k<kDXS>(K, f, im, im, om, kp, nullptr, B, H, L, 1, st)
+                     : launch_any_k<kFWD>(K, f, im, im, om, kp, nullptr, B, H, L, 1, st);
     }
+    scratch_free(kp, st);
+    return rc;
 }
 
 }  // namespace bwds

@@ -245,6 +245,9 @@ static void pick_tile(int64_t L, int64_t K, int* R, int* NT) {
     }
 }
 
+ks_status stencil_short_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t, int,
+                            int, cudaStream_t, bool*);
+
 // Sets *handled = false (and does nothing) when this path does not apply; the
 // caller then uses the generic kernels of conv_fwd.cu.
 ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
@@ -257,6 +260,10 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
         const ks_status s = env_int("KS_CB_IMPL", 0) == 1
                                 ? stencil_cb_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled)
                                 : stencil_pad_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
+        if (*handled) return s;
+    }
+    if (K <= 16 && L >= 1024 && env_int("KS_STS", 1)) {  // K-specialised short-kernel stencil (bwd_short.cuh)
+        const ks_status s = stencil_short_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }
     int R, NT;

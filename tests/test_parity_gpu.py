@@ -319,6 +319,28 @@ def test_bwd_short_equals_generic_kernels(K, monkeypatch):
         assert same(dx_s, host(ks.backward_input(gy, k, m))), m
 
 
+@pytest.mark.parametrize("K", list(range(1, 17)))
+def test_stencil_short_equals_generic_and_oracle(K, oracle, monkeypatch):
+    """The K-specialised forward / dX stencils (bwd_short.cuh, persistent grid
+    with more rows than CTAs, ragged last tile L = 2080) against the generic
+    stencil_tma they replace (KS_STS=0) bit for bit and, on sampled channels,
+    against the oracle bit for bit, in both multiply-add modes."""
+    B, H, L = 40, 16, 2080
+    x, k, gy = ks.make_inputs(12, B, H, L, K)
+    kh = k.cpu().numpy()
+    for m in (SEPARATE, FUSED):
+        monkeypatch.setenv("KS_STS", "0")
+        y_g, dx_g = host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))
+        monkeypatch.delenv("KS_STS")
+        y, dx = ks.forward(x, k, m), ks.backward_input(gy, k, m)
+        assert same(host(y), y_g), m
+        assert same(host(dx), dx_g), m
+        for h in (0, H - 1):
+            ks_ = np.ascontiguousarray(kh[h:h + 1])
+            assert same(_channel_slice(y, h), oracle.forward(_channel_slice(x, h), ks_, m)), (h, m)
+            assert same(_channel_slice(dx, h), oracle.backward_input(_channel_slice(gy, h), ks_, m)), (h, m)
+
+
 def test_fused_backward_config3_against_oracle(oracle):
     """At config 3 (4 GiB per tensor): the fused backward's dx on sampled
     channels bitwise against the oracle, dk to tolerance against fp64."""
