@@ -47,27 +47,30 @@ bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t 
     return r == CUDA_SUCCESS;
 }
 
-// Padded view: the [rows, L] tensor as the 5-D tensor {4, 8, L/32, H, rows/H}
-// (floats, quads, 32-float pieces, channels, batch entries) with box
-// {4, 9, n, 1, depth}.  Quad 8 of every piece lies outside dim 1, so TMA
-// zero-fills it and each 32-float piece lands as a 36-float shared row: the
-// bank-conflict-free padded layout with no re-layout pass.  `depth` > 1 stacks
-// the same channel of consecutive batch entries (the dW kernel); the stencil
-// uses depth 1 with H = 1 (rows = channels x batch) or stacks channels via
-// dim 3 by passing chan_box > 1.
+// Padded view: the [rows, L] tensor (rows = batch x H channels) as the 4-D
+// tensor {32, L/32, H, rows/H} (floats, 32-float pieces, channels, batch
+// entries) with box {36, n, chan_box, depth}.  The box's inner extent runs 4
+// floats past the 32-float inner dimension, so TMA fetches each 128-byte
+// piece and lands it as a 144-byte shared row (the excess quad is out of
+// bounds): the bank-conflict-free padded layout with no re-layout pass.
+// `depth` > 1 stacks the same channel of consecutive batch entries (the dW
+// kernel); chan_box > 1 stacks channels (the stencil).  This replaced a 5-D
+// view {4, 8, L/32, H, B} with box {4, 9, n, ...} that produced the same
+// shared layout from 16-byte rows and streamed at only 4.05 TB/s
+// (tools/probes/tma_box_probe.cu: 7.07 TB/s for the 128-byte-row box).
 bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
                         int chan_box, int depth) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || L % 32 != 0 || H < 1 || rows % H != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
     if (n < 1 || n > 256 || chan_box < 1 || chan_box > 256 || depth < 1 || depth > 256) return false;
     if (L / 32 >= (int64_t(1) << 31) || H >= (int64_t(1) << 31) || rows / H >= (int64_t(1) << 31)) return false;
-    const cuuint64_t dims[5] = {4, 8, static_cast<cuuint64_t>(L / 32), static_cast<cuuint64_t>(H),
+    const cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(L / 32), static_cast<cuuint64_t>(H),
                                 static_cast<cuuint64_t>(rows / H)};
-    const cuuint64_t strides[4] = {16, 128, static_cast<cuuint64_t>(L) * 4, static_cast<cuuint64_t>(L * H) * 4};
-    const cuuint32_t box[5] = {4, 9, static_cast<cuuint32_t>(n), static_cast<cuuint32_t>(chan_box),
+    const cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(L) * 4, static_cast<cuuint64_t>(L * H) * 4};
+    const cuuint32_t box[4] = {36, static_cast<cuuint32_t>(n), static_cast<cuuint32_t>(chan_box),
                                static_cast<cuuint32_t>(depth)};
-    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
-    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(base), dims, strides, box,
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -76,10 +79,9 @@ bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64
 // Padded row view: the [rows, L] tensor as {32, L/32, rows} with box
 // {36, n, 1} -- the box's inner extent runs 4 floats past the inner dimension,
 // so every 128-byte global piece lands as a 144-byte shared row (the excess
-// quad is out of bounds and never fetched).  Same padded layout as
-// encode_padded_view, but TMA moves 128-byte rows instead of 16-byte ones:
-// 7.07 TB/s streamed vs 4.05 for the 5-D view (tools/probes/tma_box_probe.cu
-// on the B200; 7.25 for the 128B-swizzled 32-float box).
+// quad is out of bounds and never fetched) -- encode_padded_view's layout for
+// a plain [rows, L] row index (7.07 TB/s streamed on the B200, 7.25 for the
+// 128B-swizzled 32-float box, tools/probes/tma_box_probe.cu).
 bool encode_row_view_padded(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int n) {
     EncodeTiledFn fn = encode_fn();
     if (!fn || L % 32 != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;

@@ -8,8 +8,8 @@
 // t-slice in 32-t chunks of two 16-t register windows: 16 gy values (4 loads)
 // and 47 x values (12 loads) feed 512 FMAs at compile-time shared offsets.
 // Work item = (row b, TT-wide t tile): TMA brings gy[t0, t0+TT) and the x
-// window as 36-float padded rows (box {4, 9, n, 1, 1} of the 5-D view, quad 8
-// zero-filled), so the CTA computes straight from an NS-stage ring with no
+// window as 36-float padded rows (box {36, n, 1, 1} of the padded view, the
+// 4 floats past each 32-float piece out of bounds and zero-filled), so the CTA computes straight from an NS-stage ring with no
 // re-layout; one producer lane keeps the ring NS items ahead (full / empty
 // mbarriers; every consumer thread arrives on a stage's empty barrier once it
 // is done with it).  The x window must start on a 32-float piece, so tap
@@ -90,10 +90,10 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                 const int r0 = (u % ntt) * (g.TT / 32);
                 unsigned char* sb = smem + stage * g.stage_bytes;
                 mbar_arrive_expect_tx(&full[stage], tx_bytes);
-                tma_load_5d(sb, &gy_map, r0, h, b, &full[stage]);
+                tma_load_pad(sb, &gy_map, r0, h, b, &full[stage]);
                 unsigned char* xb = sb + g.gy_alloc * 144;
-                tma_load_5d(xb, &x_map, r0 + xrow_rel, h, b, &full[stage]);
-                if (g.nbx > 1) tma_load_5d(xb + g.NBX * 144, &x_map, r0 + xrow_rel + g.NBX, h, b, &full[stage]);
+                tma_load_pad(xb, &x_map, r0 + xrow_rel, h, b, &full[stage]);
+                if (g.nbx > 1) tma_load_pad(xb + g.NBX * 144, &x_map, r0 + xrow_rel + g.NBX, h, b, &full[stage]);
             }
         }
         return;

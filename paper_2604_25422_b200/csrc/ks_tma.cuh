@@ -113,12 +113,13 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         : "memory");
 }
 
-// 5-D tiled TMA load (the padded view of encode_padded_view).
-__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, int c2, int c3, int c4,
+// Tiled TMA load of the padded view (encode_padded_view, 4-D {32, L/32, H, B}):
+// piece c2 of channel c3 of batch entry c4.
+__device__ __forceinline__ void tma_load_pad(void* dst, const CUtensorMap* map, int c2, int c3, int c4,
                                             uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+        "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
         : "memory");
 }
@@ -170,10 +171,10 @@ __device__ __forceinline__ uint32_t swz(uint32_t i) {
 bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int inner, int box_rows,
                      int sw);
 
-// Host: the padded 5-D view {4, 8, L/32, H, rows/H} of a [rows, L] fp32 tensor
-// (rows = batch x H channels) with box {4, 9, n, chan_box, depth}: every
-// 32-float piece lands as a 36-float shared row whose last quad is zero
-// (conflict-free 128-bit reads 144 B apart, no re-layout pass).
+// Host: the padded view {32, L/32, H, rows/H} of a [rows, L] fp32 tensor
+// (rows = batch x H channels) with box {36, n, chan_box, depth}: every
+// 32-float piece lands as a 36-float shared row (conflict-free 128-bit reads
+// 144 B apart, no re-layout pass).
 bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
                         int chan_box, int depth);
 

@@ -6,9 +6,9 @@
 // The FMA inner loop wants each thread's 32-output register tile to read its
 // input window with 128-bit loads at compile-time offsets, bank-conflict free:
 // rows of 32 floats at a 36-float (144 B) pitch.  TMA writes that layout
-// itself: the tensor is viewed as {4 floats, 8 quads, L/32 pieces, H, B} and
-// loaded with box {4, 9, n, RPT, 1} -- quad 8 lies outside dim 1 and is
-// zero-filled, so every 32-float piece lands as a 36-float row.  No re-layout
+// itself: the tensor is viewed as {32 floats, L/32 pieces, H, B} and loaded
+// with box {36, n, RPT, 1} -- floats 32..35 of every piece lie outside dim 0
+// and are zero-filled, so every 32-float piece lands as a 36-float row.  No re-layout
 // pass, no producer warp: the CTA computes straight from the stage ring.
 //
 // The window must start on a 32-float piece: the taps are given `lead` =
@@ -124,8 +124,8 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         unsigned char* sb = smem + stage * g.stage_bytes;
         mbar_arrive_expect_tx(&full[stage], tx_bytes);
         const int r0 = t0 / 32 - g.base_row;
-        tma_load_5d(sb, &in_map, r0, h0, b, &full[stage]);
-        if (g.nbox > 1) tma_load_5d(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
+        tma_load_pad(sb, &in_map, r0, h0, b, &full[stage]);
+        if (g.nbox > 1) tma_load_pad(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
         bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kp,
                   static_cast<uint32_t>(g.RPT * g.Kp) * 4u, &full[stage]);
     };
