@@ -84,23 +84,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// Wait with back-off: for a producer warp that would otherwise spin hot and
-// steal issue slots from the FMA warps it feeds.
+// Parked wait for a producer lane: try_wait with a suspend-time hint blocks
+// the thread in hardware until the phase completes (or ~1 ms passes), so the
+// producer takes no issue slots from the FMA warps it feeds.  (The previous
+// try_wait + __nanosleep(128) loop spun: at config 5b its SYNCS / BRA /
+// NANOSLEEP were 25% of all instructions issued by stencil_pad.)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
     uint32_t done;
-    for (;;) {
+    do {
         asm volatile(
             "{\n"
             ".reg .pred p;\n"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n"
             "selp.u32 %0, 1, 0, p;\n"
             "}\n"
             : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity)
+            : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
             : "memory");
-        if (done) return;
-        __nanosleep(128);
-    }
+    } while (!done);
 }
 
 // 3-D tiled TMA load of one box into shared memory, completing on `bar`.

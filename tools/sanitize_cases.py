@@ -43,7 +43,10 @@ for (B, H, L, K) in shapes:
 # 4 dW work items per CTA (> NS = 3 stages); odd p (K = 150) shifts the tap origin
 # (64,32,4096,7): fused backward (dX + dW in one pass), several work items per CTA
 # (2400,16,48,48): short-row chunks reused round the stage ring (paper shape rows)
-for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48)]:
+# (40,16,2080,16), (8,4,4160,13): K-specialised short-kernel stencils (persistent,
+# more rows than CTAs), dW and fused backward with ragged last tiles
+for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48),
+                     (40, 16, 2080, 16), (8, 4, 4160, 13)]:
     x, k, gy = o.fill_inputs(5, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
     y = ks.forward(dx_, dk_, 1)
