@@ -24,7 +24,7 @@
 //   36-float shared row, so a thread's quads sit at (piece * 144 +
 //   compile-time) bytes and every LDS.128 is [base + imm] -- conflict-free
 //   (lanes 144 B apart) with no swizzle arithmetic.  The column 8 (w & 3) is
-//   made compile-time by one warp-uniform switch at entry.
+//   made compile-time by a warp-uniform switch around each item's math.
 // * The fused kernel takes the 8 gy values of the dW block from the dX
 //   window it already holds (the dX window of a block covers gy[t, t+8)).
 // * Stage / phase / (row, tile) are carried incrementally: no integer
@@ -89,7 +89,71 @@ struct Args {
     int grp;                 // dW modes: the CTA's row group
 };
 
+// One work item's math for the thread whose block starts at column C0 of its
+// piece (C0 = 8 (w & 3), a template constant so every shared access is
+// [base + imm]); the caller switches on the warp-uniform column around this
+// call only, so all warps meet the same barrier instructions.
 template <int KT, bool FUSED, int MODE, int C0>
+__device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob, uint32_t o0, uint32_t o1,
+                                     const float (&w)[Geo<KT, MODE>::HAS_ST ? 16 : 1],
+                                     float (&acc)[Geo<KT, MODE>::HAS_DW ? KT : 1]) {
+    using Gm = Geo<KT, MODE>;
+    float gv[8];
+    if constexpr (Gm::HAS_ST) {
+        // out[t0+tl+r] = sum_j in[t0+tl+r+j-OFF] * w[j], j ascending from +0;
+        // window quad c = input logical (t0-32 origin) 32 + tl - QS + 4c
+        float v2[4 * Gm::NV2];
+#pragma unroll
+        for (int c = 0; c < Gm::NV2; ++c) {
+            const float4 qv = lds4(gys + pofs(32 + C0 - Gm::QS + 4 * c));
+            v2[4 * c + 0] = qv.x;
+            v2[4 * c + 1] = qv.y;
+            v2[4 * c + 2] = qv.z;
+            v2[4 * c + 3] = qv.w;
+        }
+        float d[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) d[r] = 0.f;
+#pragma unroll
+        for (int jj = 0; jj < KT; ++jj)
+#pragma unroll
+            for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v2[Gm::S2 + r + jj], w[jj]);
+        *reinterpret_cast<float4*>(ob + o0) = make_float4(d[0], d[1], d[2], d[3]);
+        *reinterpret_cast<float4*>(ob + o1) = make_float4(d[4], d[5], d[6], d[7]);
+        if constexpr (MODE == kFUSED) {
+#pragma unroll
+            for (int tt = 0; tt < 8; ++tt) gv[tt] = v2[Gm::QS + tt];
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const float4 qv = lds4(gys + pofs(C0 + 4 * c));
+            gv[4 * c + 0] = qv.x;
+            gv[4 * c + 1] = qv.y;
+            gv[4 * c + 2] = qv.z;
+            gv[4 * c + 3] = qv.w;
+        }
+    }
+    if constexpr (Gm::HAS_DW) {
+        // dW: x logical (origin t0 - p - D) A + tl + 4c; acc[jj] += gy[t] * x[t + jj - p]
+        const unsigned char* xs = gys + Gm::GYRegion;
+        float xv[4 * Gm::NVX];
+#pragma unroll
+        for (int c = 0; c < Gm::NVX; ++c) {
+            const float4 qv = lds4(xs + pofs(Gm::A + C0 + 4 * c));
+            xv[4 * c + 0] = qv.x;
+            xv[4 * c + 1] = qv.y;
+            xv[4 * c + 2] = qv.z;
+            xv[4 * c + 3] = qv.w;
+        }
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt)
+#pragma unroll
+            for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
+    }
+}
+
+template <int KT, bool FUSED, int MODE>
 __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap* x_map, const CUtensorMap* out_map,
                                     const float* __restrict__ k, float* __restrict__ part, unsigned char* smem,
                                     uint64_t* full, float (*red)[KT], const Args a) {
@@ -133,9 +197,10 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
 
     const int R = lane + 32 * (warp >> 2);  // piece of this thread's block within the tile
     const unsigned char* tb = stages + R * kPitch;
-    // output tile: 128B-swizzled rows of 32 floats, this thread's 8 outputs at row R, quads C0/4, C0/4+1
-    const uint32_t o0 = static_cast<uint32_t>(R * 128 + (((C0 / 4) ^ (R & 7)) << 4));
-    const uint32_t o1 = static_cast<uint32_t>(R * 128 + (((C0 / 4 + 1) ^ (R & 7)) << 4));
+    const int cw = warp & 3;                // the block's column is 8 cw
+    // output tile: 128B-swizzled rows of 32 floats, this thread's 8 outputs at row R, quads 2 cw, 2 cw + 1
+    const uint32_t o0 = static_cast<uint32_t>(R * 128 + (((2 * cw) ^ (R & 7)) << 4));
+    const uint32_t o1 = static_cast<uint32_t>(R * 128 + (((2 * cw + 1) ^ (R & 7)) << 4));
 
     int stage = 0, t0 = 0, row = a.row0;
     uint32_t phase = 0;
@@ -155,58 +220,11 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
             }
         }
         if (t0 + 32 * R < a.L) {
-            float gv[8];
-            if constexpr (Gm::HAS_ST) {
-                // out[t0+tl+r] = sum_j in[t0+tl+r+j-OFF] * w[j], j ascending from +0;
-                // window quad c = input logical (t0-32 origin) 32 + tl - QS + 4c
-                float v2[4 * Gm::NV2];
-#pragma unroll
-                for (int c = 0; c < Gm::NV2; ++c) {
-                    const float4 qv = lds4(gys + pofs(32 + C0 - Gm::QS + 4 * c));
-                    v2[4 * c + 0] = qv.x;
-                    v2[4 * c + 1] = qv.y;
-                    v2[4 * c + 2] = qv.z;
-                    v2[4 * c + 3] = qv.w;
-                }
-                float d[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) d[r] = 0.f;
-#pragma unroll
-                for (int jj = 0; jj < KT; ++jj)
-#pragma unroll
-                    for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v2[Gm::S2 + r + jj], w[jj]);
-                *reinterpret_cast<float4*>(ob + o0) = make_float4(d[0], d[1], d[2], d[3]);
-                *reinterpret_cast<float4*>(ob + o1) = make_float4(d[4], d[5], d[6], d[7]);
-                if constexpr (MODE == kFUSED) {
-#pragma unroll
-                    for (int tt = 0; tt < 8; ++tt) gv[tt] = v2[Gm::QS + tt];
-                }
-            } else {
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const float4 qv = lds4(gys + pofs(C0 + 4 * c));
-                    gv[4 * c + 0] = qv.x;
-                    gv[4 * c + 1] = qv.y;
-                    gv[4 * c + 2] = qv.z;
-                    gv[4 * c + 3] = qv.w;
-                }
-            }
-            if constexpr (Gm::HAS_DW) {
-                // dW: x logical (origin t0 - p - D) A + tl + 4c; acc[jj] += gy[t] * x[t + jj - p]
-                const unsigned char* xs = gys + Gm::GYRegion;
-                float xv[4 * Gm::NVX];
-#pragma unroll
-                for (int c = 0; c < Gm::NVX; ++c) {
-                    const float4 qv = lds4(xs + pofs(Gm::A + C0 + 4 * c));
-                    xv[4 * c + 0] = qv.x;
-                    xv[4 * c + 1] = qv.y;
-                    xv[4 * c + 2] = qv.z;
-                    xv[4 * c + 3] = qv.w;
-                }
-#pragma unroll
-                for (int tt = 0; tt < 8; ++tt)
-#pragma unroll
-                    for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
+            switch (cw) {
+                case 0: item<KT, FUSED, MODE, 0>(gys, ob, o0, o1, w, acc); break;
+                case 1: item<KT, FUSED, MODE, 8>(gys, ob, o0, o1, w, acc); break;
+                case 2: item<KT, FUSED, MODE, 16>(gys, ob, o0, o1, w, acc); break;
+                default: item<KT, FUSED, MODE, 24>(gys, ob, o0, o1, w, acc); break;
             }
         }
         if constexpr (Gm::HAS_ST) {
@@ -297,12 +315,7 @@ bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         fence_mbar_init();
     }
     __syncthreads();
-    switch ((threadIdx.x >> 5) & 3) {  // warp-uniform: the block's column 8 (w & 3) becomes a constant
-        case 0: run<KT, FUSED, MODE, 0>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
-        case 1: run<KT, FUSED, MODE, 8>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
-        case 2: run<KT, FUSED, MODE, 16>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
-        default: run<KT, FUSED, MODE, 24>(&in_map, &x_map, &out_map, k, part, smem, full, red, a); break;
-    }
+    run<KT, FUSED, MODE>(&in_map, &x_map, &out_map, k, part, smem, full, red, a);
 }
 
 }  // namespace bwds

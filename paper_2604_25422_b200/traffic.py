@@ -17,7 +17,7 @@ model) extends to B200:
   (TMA boxes overlap by 32*HH floats per side per tile);
 * ``plan(path, B, H, L, K)`` -- which kernel family runs, its tile and grid
   (mirrors the host dispatch in csrc/: conv_fwd.cu, stencil_tma.cu,
-  stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
+  bwd_short.cuh, stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
 
 ``tests/test_traffic.py`` checks memory_traffic against the ncu DRAM bytes
 committed in profiles/ncu_summary.json.
@@ -42,6 +42,8 @@ def _stencil_tier(L: int, K: int):
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
     if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
+    if K <= 16 and L >= 1024:
+        return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
     if L >= 1024:
         nt = 256 if L >= 4096 and K <= 8 else 128 if L >= 2048 else 64
         return "stencil_tma", 16, nt
@@ -64,11 +66,13 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
     G = max(1, min(math.ceil(8192 / (H * njt)), B))
     if L < 2048 and L % 4 == 0:
         return "dw_rows", G
+    if L % 32 == 0 and K <= 16:
+        return "dw_short", G  # bwd_short.cuh MODE dW: dw_tma's decomposition, K-specialised
     return ("dw_tma" if L % 32 == 0 else "dw_hier_stage1"), G
 
 
 def bwd_fused_applies(L: int, K: int) -> bool:
-    """ks_dwconv1d_bwd_f32 runs the one-pass kernel (csrc/dw_tma.cu BWD)."""
+    """ks_dwconv1d_bwd_f32 runs the one-pass kernel (csrc/bwd_short.cuh MODE fused)."""
     return L % 32 == 0 and L >= 2048 and K <= 16
 
 
@@ -78,7 +82,7 @@ def plan(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical"
     if path == "bwd":
         if bwd_fused_applies(L, K):
             _, G = _dw_groups(B, H, L, K)
-            return {"kernel": "dw_tma_bwd", "row_groups": G, "partials_bytes": 4 * G * H * K}
+            return {"kernel": "bwd_short", "row_groups": G, "partials_bytes": 4 * G * H * K}
         return {"kernel": "split", "dx": plan("dx", B, H, L, K), "dw": plan("dw", B, H, L, K)}
     if path in ("fwd", "dx"):
         name, R, NT = _stencil_tier(L, K)
@@ -102,8 +106,9 @@ def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hie
     base = logical_traffic(path, B, H, L, K)
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
-        kp = 4 * H * (math.ceil(K / 32) * 32)  # prep_taps writes kp, the kernel reads it back
-        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad") else 0)
+        kp = 4 * H * (16 if p["kernel"] == "stencil_short" else math.ceil(K / 32) * 32)
+        # prep_taps writes kp, the kernel reads it back
+        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short") else 0)
     if p["kernel"] == "dw_pairwise_tma":
         return base
     return base + 2 * p["partials_bytes"]  # partials written by stage 1, read by stage 2
@@ -116,6 +121,6 @@ def l2_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
     if path not in ("fwd", "dx") or not p["tiles"]:
         return memory_traffic(path, B, H, L, K)
     off = K // 2 if path == "fwd" else K - 1 - K // 2
-    HH = max(1, math.ceil(max(off, K - 1 - off) / 32))
+    HH = 1 if p["kernel"] == "stencil_short" else max(1, math.ceil(max(off, K - 1 - off) / 32))
     halo = p["tiles"] * 2 * 32 * HH * 4
     return memory_traffic(path, B, H, L, K) + halo

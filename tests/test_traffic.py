@@ -14,17 +14,17 @@ def test_logical_traffic_matches_reference_formula():
 
 
 def test_plan_dispatch_tiers():
-    assert traffic.plan("fwd", 256, 512, 8192, 7)["kernel"] == "stencil_tma"
+    assert traffic.plan("fwd", 256, 512, 8192, 7)["kernel"] == "stencil_short"
     assert traffic.plan("fwd", 64, 128, 4096, 4096)["kernel"] == "stencil_pad"
     assert traffic.plan("fwd", 16384, 128, 48, 48)["kernel"] == "stencil_rows"
     assert traffic.plan("dw", 64, 128, 4096, 4096)["kernel"] == "dw_pad"
-    assert traffic.plan("dw", 256, 512, 8192, 7)["kernel"] == "dw_tma"
+    assert traffic.plan("dw", 256, 512, 8192, 7)["kernel"] == "dw_short"
     assert traffic.plan("dw", 256, 512, 8192, 7, "pairwise")["kernel"] == "dw_pairwise_tma"
 
 
 def test_fused_backward_moves_three_quarters():
     B, H, L, K = 256, 512, 8192, 7
-    assert traffic.plan("bwd", B, H, L, K)["kernel"] == "dw_tma_bwd"
+    assert traffic.plan("bwd", B, H, L, K)["kernel"] == "bwd_short"
     assert traffic.plan("bwd", 64, 128, 4096, 4096)["kernel"] == "split"
     split = traffic.memory_traffic("dx", B, H, L, K) + traffic.memory_traffic("dw", B, H, L, K)
     assert abs(traffic.memory_traffic("bwd", B, H, L, K) / split - 0.75) < 0.01

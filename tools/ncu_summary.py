@@ -117,15 +117,28 @@ def main():
     if a.launches:
         per = launches(a.launches, a.round)
         # per-path DRAM bytes from the last complete fwd/dX/dW triple
-        def is_bwd(n):  # dw_tma<JR, TB, NJ, S, FUSED, BWD, S2>: the fused backward
+        def short_mode(n):  # bwd_short<K, FUSED, MODE>: 0 dW, 1 fused backward, 2 fwd, 3 dX
+            if "bwd_short<" not in n:
+                return None
+            args = n.split("bwd_short<", 1)[1].split(">", 1)[0].split(",")
+            return int(args[2]) if len(args) >= 3 else None
+
+        def is_bwd(n):  # the fused backward: bwd_short MODE 1, or dw_tma<JR, TB, NJ, S, FUSED, BWD, S2>
+            if short_mode(n) is not None:
+                return short_mode(n) == 1
             if "dw_tma<" not in n:
                 return False
             args = n.split("dw_tma<", 1)[1].split(">", 1)[0].split(",")
             return len(args) >= 6 and args[5].strip() in ("1", "true")
 
-        stencil = [m for (i, n, g, b), m in sorted(per.items()) if "stencil" in n or "conv_tile" in n]
-        dw = [m for (i, n, g, b), m in sorted(per.items())
-              if ("dw_tma" in n or "dw_hier" in n) and not is_bwd(n)]
+        def is_stencil(n):
+            return "stencil" in n or "conv_tile" in n or short_mode(n) in (2, 3)
+
+        def is_dw(n):
+            return ("dw_tma" in n or "dw_hier" in n or short_mode(n) == 0) and not is_bwd(n)
+
+        stencil = [m for (i, n, g, b), m in sorted(per.items()) if is_stencil(n)]
+        dw = [m for (i, n, g, b), m in sorted(per.items()) if is_dw(n)]
         bwd = [m for (i, n, g, b), m in sorted(per.items()) if is_bwd(n)]
         if bwd:
             m = bwd[-1]
@@ -134,9 +147,8 @@ def main():
         # with the fused-backward step the list ends ... fwd, dX, dW | fwd, bwd:
         # take fwd and dX from the last split step (the stencils before the last dW)
         if bwd and dw:
-            last_dw = max(i for (i, n, g, b) in per if ("dw_tma" in n or "dw_hier" in n) and not is_bwd(n))
-            stencil = [m for (i, n, g, b), m in sorted(per.items())
-                       if ("stencil" in n or "conv_tile" in n) and i < last_dw]
+            last_dw = max(i for (i, n, g, b) in per if is_dw(n))
+            stencil = [m for (i, n, g, b), m in sorted(per.items()) if is_stencil(n) and i < last_dw]
         if len(stencil) >= 2:
             for name, m in (("fwd", stencil[-2]), ("dX", stencil[-1])):
                 cfg[name] = {"dram_bytes": int(m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]),
