@@ -42,6 +42,7 @@ constexpr int kDW = 0;      // HIERARCHICAL dW stage 1 (part[G,H,K])
 constexpr int kFUSED = 1;   // dX + dW stage 1 from one pass over gy and x
 constexpr int kFWD = 2;     // forward stencil: out = x (*) k, offset p
 constexpr int kDXS = 3;     // dX stencil: out = gy (*) reversed k, offset q
+constexpr int kDirect = 8;  // | kDirect: stencil outputs go straight to HBM (one 256-bit store per 8 outputs)
 
 constexpr int kThreads = 256;
 constexpr int kTT = 2048;                // t per work item
@@ -52,28 +53,31 @@ constexpr int kOutBytes = kTT * 4;       // one output tile, 128B-swizzled rows
 
 template <int KT, int MODE>
 struct Geo {
-    static constexpr bool HAS_DW = MODE <= kFUSED;  // x window + dW accumulators
-    static constexpr bool HAS_ST = MODE >= kFUSED;  // a stencil output tile per item
+    static constexpr int BASE = MODE & 7;             // kDW / kFUSED / kFWD / kDXS
+    static constexpr bool DST = (MODE & kDirect) != 0;  // stencil output stored straight from registers
+    static constexpr bool HAS_DW = BASE <= kFUSED;  // x window + dW accumulators
+    static constexpr bool HAS_ST = BASE >= kFUSED;  // a stencil output tile per item
     static constexpr int p = KT / 2;
     static constexpr int q = KT - 1 - p;                  // dX offset (src/conv_core.cpp:56)
     static constexpr int D = (32 - p % 32) % 32;          // x window origin t0 - p - D on a piece
     static constexpr int A = D & ~3;
     static constexpr int S = D & 3;                       // (-p) mod 4
     static constexpr int XR0 = (p + D) / 32;              // x window first piece = t0/32 - XR0
-    static constexpr int OFF = MODE == kFWD ? p : q;      // stencil offset
+    static constexpr int OFF = BASE == kFWD ? p : q;      // stencil offset
     static constexpr int S2 = (4 - OFF % 4) % 4;          // (-OFF) mod 4
     static constexpr int QS = OFF + S2;                   // multiple of 4
     static constexpr int NVX = (S + 8 + KT - 1 + 3) / 4;  // x quads per block
     static constexpr int NV2 = (S2 + 8 + KT - 1 + 3) / 4; // stencil window quads per block
-    static constexpr int GYP = MODE == kDW ? 64 : 66;     // stencil input: one halo piece each side
+    static constexpr int GYP = BASE == kDW ? 64 : 66;     // stencil input: one halo piece each side
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
-    static constexpr int TapBytes = MODE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
+    static constexpr int TapBytes = BASE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
     static constexpr int Stage = GYRegion + (HAS_DW ? kXRegion : 0) + TapBytes;
-    static constexpr int NS = MODE >= kFWD ? 4 : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
-    static constexpr int MinBlocks = MODE >= kFWD ? 4 : 3;
+    static constexpr int NS = BASE >= kFWD ? 4 : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
+    static constexpr int MinBlocks = BASE >= kFWD ? 4 : 3;
     static constexpr uint32_t TX =
-        static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (MODE >= kFWD ? 64 : 0));
-    static constexpr int Smem = (HAS_ST ? 2 * kOutBytes : 0) + NS * Stage + 64 + 1024;
+        static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 64 : 0));
+    static constexpr bool HAS_OBUF = HAS_ST && !DST;  // output tiles leave by TMA store from shared memory
+    static constexpr int Smem = (HAS_OBUF ? 2 * kOutBytes : 0) + NS * Stage + 64 + 1024;
     static_assert(QS % 4 == 0 && QS + 8 <= 4 * NV2, "gy block inside the dX window");
     static_assert(A + 2040 + 4 * NVX <= kXP * 32, "x window inside the staged pieces");
     static_assert(!HAS_ST || 32 + 2040 - QS + 4 * NV2 <= GYP * 32, "stencil window inside the staged pieces");
@@ -82,8 +86,16 @@ struct Geo {
 // byte offset of the quad at logical index e (>= 0, 4-aligned) from a piece base
 __host__ __device__ constexpr int pofs(int e) { return (e >> 5) * kPitch + (e & 31) * 4; }
 
+// 256-bit global store (STG.E.256 on sm_100): 8 floats = one whole 32-byte sector
+__device__ __forceinline__ void st_v8(float* p, const float (&d)[8]) {
+    asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p), "f"(d[0]), "f"(d[1]), "f"(d[2]),
+                 "f"(d[3]), "f"(d[4]), "f"(d[5]), "f"(d[6]), "f"(d[7])
+                 : "memory");
+}
+
 struct Args {
     int H, L;
+    float* out;              // kDirect: the stencil output tensor
     int row0, rstep, nrows;  // this CTA's rows: row0 + i * rstep, i < nrows (row = b * H + h)
     int h;                   // dW modes: the CTA's channel
     int grp;                 // dW modes: the CTA's row group
@@ -94,7 +106,7 @@ struct Args {
 // [base + imm]); the caller switches on the warp-uniform column around this
 // call only, so all warps meet the same barrier instructions.
 template <int KT, bool FUSED, int MODE, int C0>
-__device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob, uint32_t o0, uint32_t o1,
+__device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob, uint32_t o0, uint32_t o1, float* gout,
                                      const float (&w)[Geo<KT, MODE>::HAS_ST ? 16 : 1],
                                      float (&acc)[Geo<KT, MODE>::HAS_DW ? KT : 1]) {
     using Gm = Geo<KT, MODE>;
@@ -118,9 +130,13 @@ __device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob
         for (int jj = 0; jj < KT; ++jj)
 #pragma unroll
             for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v2[Gm::S2 + r + jj], w[jj]);
-        *reinterpret_cast<float4*>(ob + o0) = make_float4(d[0], d[1], d[2], d[3]);
-        *reinterpret_cast<float4*>(ob + o1) = make_float4(d[4], d[5], d[6], d[7]);
-        if constexpr (MODE == kFUSED) {
+        if constexpr (Gm::DST) {
+            st_v8(gout, d);  // the block's 8 outputs = one whole 32-byte sector
+        } else {
+            *reinterpret_cast<float4*>(ob + o0) = make_float4(d[0], d[1], d[2], d[3]);
+            *reinterpret_cast<float4*>(ob + o1) = make_float4(d[4], d[5], d[6], d[7]);
+        }
+        if constexpr (Gm::BASE == kFUSED) {
 #pragma unroll
             for (int tt = 0; tt < 8; ++tt) gv[tt] = v2[Gm::QS + tt];
         }
@@ -163,7 +179,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     const int warp = tid >> 5, lane = tid & 31;
     const int ntt = (a.L + kTT - 1) / kTT;
     const int nunits = a.nrows * ntt;
-    unsigned char* stages = smem + (Gm::HAS_ST ? 2 * kOutBytes : 0);
+    unsigned char* stages = smem + (Gm::HAS_OBUF ? 2 * kOutBytes : 0);
 
     // producer state (thread 0): next item to load
     int irow = a.row0, it0 = 0;
@@ -171,9 +187,9 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         uint64_t* bar = &full[stage];
         unsigned char* sb = stages + stage * Gm::Stage;
         mbar_arrive_expect_tx(bar, Gm::TX);
-        tma_load_3d(sb, in_map, 0, it0 / 32 - (MODE == kDW ? 0 : 1), irow, bar);
+        tma_load_3d(sb, in_map, 0, it0 / 32 - (Gm::BASE == kDW ? 0 : 1), irow, bar);
         if constexpr (Gm::HAS_DW) tma_load_3d(sb + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, irow, bar);
-        if constexpr (MODE >= kFWD) bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * 16, 64, bar);
+        if constexpr (Gm::BASE >= kFWD) bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * 16, 64, bar);
         it0 += kTT;
         if (it0 >= a.L) {
             it0 = 0;
@@ -187,7 +203,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     // registers; the stencils read the row's prepared taps (prep_taps:
     // reversed for dX, zero past K) from each stage
     float w[Gm::HAS_ST ? 16 : 1];
-    if constexpr (MODE == kFUSED) {
+    if constexpr (Gm::BASE == kFUSED) {
 #pragma unroll
         for (int jj = 0; jj < KT; ++jj) w[jj] = k[static_cast<int64_t>(a.h) * KT + KT - 1 - jj];
     }
@@ -208,7 +224,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         mbar_wait(&full[stage], phase);
         const unsigned char* gys = tb + stage * Gm::Stage;
         unsigned char* ob = smem + (u & 1) * kOutBytes;
-        if constexpr (MODE >= kFWD) {
+        if constexpr (Gm::BASE >= kFWD) {
             const float* tp = reinterpret_cast<const float*>(stages + stage * Gm::Stage + Gm::GYRegion);
 #pragma unroll
             for (int c = 0; c < (KT + 3) / 4; ++c) {
@@ -220,20 +236,21 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
             }
         }
         if (t0 + 32 * R < a.L) {
+            float* gout = Gm::DST ? a.out + static_cast<int64_t>(row) * a.L + t0 + 32 * R + 8 * cw : nullptr;
             switch (cw) {
-                case 0: item<KT, FUSED, MODE, 0>(gys, ob, o0, o1, w, acc); break;
-                case 1: item<KT, FUSED, MODE, 8>(gys, ob, o0, o1, w, acc); break;
-                case 2: item<KT, FUSED, MODE, 16>(gys, ob, o0, o1, w, acc); break;
-                default: item<KT, FUSED, MODE, 24>(gys, ob, o0, o1, w, acc); break;
+                case 0: item<KT, FUSED, MODE, 0>(gys, ob, o0, o1, gout, w, acc); break;
+                case 1: item<KT, FUSED, MODE, 8>(gys, ob, o0, o1, gout, w, acc); break;
+                case 2: item<KT, FUSED, MODE, 16>(gys, ob, o0, o1, gout, w, acc); break;
+                default: item<KT, FUSED, MODE, 24>(gys, ob, o0, o1, gout, w, acc); break;
             }
         }
-        if constexpr (Gm::HAS_ST) {
+        if constexpr (Gm::HAS_OBUF) {
             fence_proxy_async_smem();           // output tile visible to the TMA store
             if (tid == 0) bulk_wait_read_all();  // store u-1 has read buffer (u+1)&1
         }
         __syncthreads();
         if (tid == 0) {
-            if constexpr (Gm::HAS_ST) {
+            if constexpr (Gm::HAS_OBUF) {
                 tma_store_3d(out_map, ob, 0, t0 / 32, row);  // columns past L are clipped
                 bulk_commit();
             }
@@ -249,7 +266,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
             row += a.rstep;
         }
     }
-    if (Gm::HAS_ST && tid == 0) bulk_wait_all();
+    if (Gm::HAS_OBUF && tid == 0) bulk_wait_all();
 
     if constexpr (Gm::HAS_DW) {
         // fixed xor-shuffle tree per warp, then the 8 warps in ascending order (as dw_tma)
@@ -280,16 +297,17 @@ template <int KT, bool FUSED, int MODE>
 __global__ void __launch_bounds__(kThreads, Geo<KT, MODE>::MinBlocks)  // 3 CTAs/SM (<= 80 regs), stencils 4
 bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap x_map,
           const __grid_constant__ CUtensorMap out_map, const float* __restrict__ k, float* __restrict__ part, int B,
-          int H, int L, int G) {
+          int H, int L, int G, float* __restrict__ out) {
     using Gm = Geo<KT, MODE>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (Gm::HAS_ST ? 2 * kOutBytes : 0) + Gm::NS * Gm::Stage);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + (Gm::HAS_OBUF ? 2 * kOutBytes : 0) + Gm::NS * Gm::Stage);
     __shared__ float red[Gm::HAS_DW ? kThreads / 32 : 1][KT];
 
     Args a;
     a.H = H;
     a.L = L;
+    a.out = out;
     if constexpr (Gm::HAS_DW) {
         a.h = blockIdx.x % H;
         a.grp = blockIdx.x / H;
@@ -310,7 +328,7 @@ bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     if (threadIdx.x == 0) {
         prefetch_tmap(&in_map);
         if (Gm::HAS_DW) prefetch_tmap(&x_map);
-        if (Gm::HAS_ST) prefetch_tmap(&out_map);
+        if (Gm::HAS_OBUF) prefetch_tmap(&out_map);
         for (int s = 0; s < Gm::NS; ++s) mbar_init(&full[s], 1);
         fence_mbar_init();
     }

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "bwd_short.cuh"
 
@@ -15,35 +16,52 @@ namespace bwds {
 
 template <int KT, bool FUSED, int MODE>
 ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k, float* part,
-                   int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
+                   int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st) {
     auto kern = bwd_short<KT, FUSED, MODE>;
     constexpr int smem = Geo<KT, MODE>::Smem;
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
-    const int64_t blocks = MODE <= kFUSED ? int64_t(G) * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
+    const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
     kern<<<static_cast<unsigned>(blocks), kThreads, smem, st>>>(im, xm, om, k, part, static_cast<int>(B),
-                                                                static_cast<int>(H), static_cast<int>(L), G);
+                                                                static_cast<int>(H), static_cast<int>(L), G, out);
     return check_launch();
 }
 
 template <int KT, int MODE>
 ks_status launch_m(bool fused, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k,
-                   float* part, int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
-    return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, st)
-                 : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, st);
+                   float* part, int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st) {
+    return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st)
+                 : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
 }
 
 template <int MODE>
 ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om,
-                       const float* k, float* part, int64_t B, int64_t H, int64_t L, int G, cudaStream_t st) {
+                       const float* k, float* part, int64_t B, int64_t H, int64_t L, int G, float* out,
+                       cudaStream_t st) {
     switch (K) {
 #define KS_BWDS_CASE(KV) \
-    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, st);
+    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, out, st);
         KS_BWDS_CASE(1) KS_BWDS_CASE(2) KS_BWDS_CASE(3) KS_BWDS_CASE(4) KS_BWDS_CASE(5) KS_BWDS_CASE(6)
         KS_BWDS_CASE(7) KS_BWDS_CASE(8) KS_BWDS_CASE(9) KS_BWDS_CASE(10) KS_BWDS_CASE(11) KS_BWDS_CASE(12)
         KS_BWDS_CASE(13) KS_BWDS_CASE(14) KS_BWDS_CASE(15) KS_BWDS_CASE(16)
 #undef KS_BWDS_CASE
         default: return KS_ERR_CUDA;
     }
+}
+
+// Stencil outputs straight from registers (one 256-bit store = one 32-byte
+// sector per thread and block) instead of a TMA store of the staged tile.
+// An A/B knob, off by default: on the B200 (tools/time_paths.py, bench.py)
+// direct stores won at (256,512,8192,K >= 11) (K = 16: fwd 1.49 -> 1.38 ms)
+// but lost at K <= 9 (K = 7: 1.45 -> 1.49 ms), in the fused backward (K = 16:
+// 1.89 -> 2.22 ms) and at config 5a's full size (fwd 11.1 -> 13.4 ms in the
+// bench, ABAB).  KS_DST=1 turns them on (both paths give the same bits).
+inline bool direct_store(const float* out, int64_t K, bool stencil) {
+    const char* e = getenv("KS_DST");
+    const int knob = e && *e ? atoi(e) : -1;
+    (void)K;
+    (void)stencil;
+    const bool on = knob > 0;
+    return on && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 }
 
 inline bool shape_ok(int64_t B, int64_t H, int64_t L, int64_t K) {
@@ -67,8 +85,9 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
     }
     *handled = true;
     const bool f = mode == KS_MULADD_FUSED;
-    return DX ? launch_any_k<kFUSED>(K, f, gm, xm, dm, k, part, B, H, L, G, st)
-              : launch_any_k<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, st);
+    if constexpr (!DX) return launch_any_k<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, nullptr, st);
+    else return direct_store(dx, K, false) ? launch_any_k<kFUSED | kDirect>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st)
+                            : launch_any_k<kFUSED>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st);
 }
 
 // Forward (reverse = 0, off = p) or dX (reverse = 1, off = q) stencil.
@@ -89,8 +108,12 @@ inline ks_status launch_stencil_short(const float* in, const float* k, float* ou
     rc = check_launch();
     if (rc == KS_OK) {
         const bool f = mode == KS_MULADD_FUSED;
-        rc = reverse ? launch_any_k<kDXS>(K, f, im, im, om, kp, nullptr, B, H, L, 1, st)
-                     : launch_any_k<kFWD>(K, f, im, im, om, kp, nullptr, B, H, L, 1, st);
+        if (direct_store(out, K, true))
+            rc = reverse ? launch_any_k<kDXS | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st)
+                         : launch_any_k<kFWD | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
+        else
+            rc = reverse ? launch_any_k<kDXS>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st)
+                         : launch_any_k<kFWD>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
     }
     scratch_free(kp, st);
     return rc;

@@ -341,6 +341,22 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle, monkeypatch):
             assert same(_channel_slice(dx, h), oracle.backward_input(_channel_slice(gy, h), ks_, m)), (h, m)
 
 
+@pytest.mark.parametrize("K", [1, 4, 7, 10, 13, 16])
+def test_short_kernels_both_output_paths(K, monkeypatch):
+    """The short-kernel stencils and fused backward write their outputs either
+    by TMA store of a staged tile or straight from registers (256-bit stores);
+    both paths give the same bits (KS_DST=0 / 1 force each)."""
+    B, H, L = 40, 16, 4160
+    x, k, gy = ks.make_inputs(13, B, H, L, K)
+    res = {}
+    for d in ("0", "1"):
+        monkeypatch.setenv("KS_DST", d)
+        dx, dk = ks.backward(gy, x, k, FUSED)
+        res[d] = [host(ks.forward(x, k, FUSED)), host(ks.backward_input(gy, k, SEPARATE)), host(dx), host(dk)]
+    for a, b in zip(res["0"], res["1"]):
+        assert same(a, b)
+
+
 def test_fused_backward_config3_against_oracle(oracle):
     """At config 3 (4 GiB per tensor): the fused backward's dx on sampled
     channels bitwise against the oracle, dk to tolerance against fp64."""
