@@ -104,12 +104,27 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     for (int i = 0; i < kJR; ++i) acc[i] = 0.f;
 
     const int nchunks = g.TT / 32;
+    // this warp's lanes: tap groups [jgw, jgw + JGW) x t-slices [ts_lo, ts_lo + TSW)
+    constexpr int JGW = NTS >= 32 ? 1 : 32 / NTS;
+    constexpr int TSW = NTS >= 32 ? 32 : NTS;
+    const int jgw = (tid & ~31) / NTS;
+    const int ts_lo = NTS >= 32 ? (tid & ~31) % NTS : 0;
+    const int xw_lo = j0 + 32 * jgw - p + 32 * ts_lo;                         // + t0 of the chunk row
+    const int xw_hi = j0 + 32 * (jgw + JGW) - 1 - p + 32 * (ts_lo + TSW) - 1;  // (chunk base i * NTS)
     for (int u = 0; u < nunits; ++u) {
         const int stage = u % NS;
         mbar_wait(&full[stage], static_cast<uint32_t>((u / NS) & 1));
         const float* pg = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const float* px = pg + g.gy_alloc * 36;
+        const int tu = (u % ntt) * g.TT;
         for (int c = ts; c < nchunks; c += NTS) {
+            // skip the chunk when, for the whole warp, every x it would read is
+            // zero halo: gy * 0 never changes a sum that starts at +0 (and the
+            // reference's WeightTerm skips those terms).  x positions are
+            // t + j - p over the warp's chunks and taps.
+            const int cb = tu + 32 * (c - ts);
+            const int xlo = cb + xw_lo, xhi = cb + xw_hi;
+            if (xhi < 0 || xlo >= L) continue;
             const float* gb = pg + c * 36;         // padded row c of the gy tile
             const float* xb = px + (c + jg) * 36;  // padded row c + jg of the x window
             auto window = [&](const int sub) {

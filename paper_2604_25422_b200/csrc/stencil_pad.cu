@@ -47,6 +47,7 @@ struct PadGeom {
     int Kp;            // taps (with lead zeros) padded to a multiple of 32
     int Ke;            // taps incl. lead zeros (the live ones)
     int base_row;      // (off + lead) / 32: window origin = t0/32 - base_row
+    int off, zlead;    // stencil offset, leading zero taps (tap block jb covers j = 32 jb - zlead ...)
     int win_floats;    // RPT * nbox * NB * 36
     int stage_bytes;   // window + RPT tap rows, 1024-aligned
 };
@@ -57,7 +58,8 @@ struct PadGeom {
 // offset of its first tap.  Each 16-tap register window takes
 // ceil((S + 47) / 4) 128-bit loads (12 for S <= 1, 13 otherwise).
 template <int S, bool FUSED>
-__device__ __forceinline__ void tile32(const float* pw, const float* wk, int pbase, int Ke, float (&acc)[kR]) {
+__device__ __forceinline__ void tile32(const float* pw, const float* wk, int pbase, int Ke, int jb_lo, int jb_hi,
+                                       float (&acc)[kR]) {
     constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
 #pragma unroll
     for (int r = 0; r < kR; ++r) acc[r] = 0.f;
@@ -87,13 +89,17 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
                 for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[S + r + jj], w[jj]);
             }
     };
+    // 32-tap blocks [jb_lo, jb_hi) only: the caller drops blocks whose every
+    // tap lands in the zero halo for the whole warp (x*0 never changes a chain
+    // that starts at +0, and the reference skips those taps anyway)
     const int Kfull = Ke & ~31;
-    for (int j0 = 0; j0 < Kfull; j0 += 32) {
+    const int jend = min(Kfull, jb_hi * 32);
+    for (int j0 = jb_lo * 32; j0 < jend; j0 += 32) {
         const float* b0 = pw + pbase + (j0 >> 5) * 36;
         window(b0, 0, wk + j0, kJS);
         window(b0, 16, wk + j0 + 16, kJS);
     }
-    if (Kfull < Ke) {
+    if (Kfull < Ke && (Kfull >> 5) >= jb_lo && (Kfull >> 5) < jb_hi) {
         const float* b0 = pw + pbase + (Kfull >> 5) * 36;
         const int rem = Ke - Kfull;
         window(b0, 0, wk + Kfull, rem < kJS ? rem : kJS);
@@ -169,8 +175,15 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         const int rg = tile / tiles_per_row;
         const int t0 = (tile - rg * tiles_per_row) * T;
         const bool live = t0 + lt * kR < L;  // L % 32 == 0: a register tile is wholly in or out
+        // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
+        // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
+        const int tw = t0 + (lt & ~31) * kR;
+        const int jb_lo = max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64);
+        const int jb_hi = (L + g.off + g.zlead - tw + 31) / 32;
         float acc[kR];
-        if (live) tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, acc);
+        if (live)
+            tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, jb_lo, jb_hi,
+                             acc);
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
         } else {
@@ -244,6 +257,8 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.Ke = static_cast<int>(K) + zlead;
     g.Kp = (g.Ke + 31) / 32 * 32;
     g.base_row = static_cast<int>((off + lead) / 32);
+    g.off = static_cast<int>(off);
+    g.zlead = zlead;
     g.RPT = 1;
     while (g.RPT < 8 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
     g.TPR = NT / g.RPT;

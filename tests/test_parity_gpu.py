@@ -257,7 +257,8 @@ def test_full_config_channel_slices(oracle, cfg):
 
 
 @pytest.mark.parametrize("shape", [(24, 256, 2048, 128), (6, 128, 16384, 64), (40, 64, 2048, 300),
-                                   (8, 32, 4096, 77), (4, 16, 2048, 1000), (4, 8, 2048, 58)])
+                                   (8, 32, 4096, 77), (4, 16, 2048, 1000), (4, 8, 2048, 58),
+                                   (4, 8, 4096, 4096), (3, 4, 2048, 3001), (2, 4, 8192, 5000)])
 def test_padded_view_kernels_many_tiles(oracle, shape):
     """Compute-bound kernels fed by the padded TMA view (stencil_pad, dw_pad)
     with several tiles / work items per CTA, so every stage and both mbarrier
