@@ -34,6 +34,17 @@
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
+// experiment knobs (compile-time; the defaults are the measured choice)
+#ifndef KS_ST_NS
+#define KS_ST_NS 4      // stencil stages
+#endif
+#ifndef KS_ST_MINB
+#define KS_ST_MINB 4    // stencil CTAs per SM (launch bounds)
+#endif
+#ifndef KS_EVICT_FIRST
+#define KS_EVICT_FIRST 0  // 1: TMA loads / stores carry an L2 evict_first policy
+#endif
+
 namespace ks {
 namespace bwds {
 
@@ -72,8 +83,8 @@ struct Geo {
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
     static constexpr int TapBytes = BASE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
     static constexpr int Stage = GYRegion + (HAS_DW ? kXRegion : 0) + TapBytes;
-    static constexpr int NS = BASE >= kFWD ? 4 : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
-    static constexpr int MinBlocks = BASE >= kFWD ? 4 : 3;
+    static constexpr int NS = BASE >= kFWD ? KS_ST_NS : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
+    static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : 3;
     static constexpr uint32_t TX =
         static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 64 : 0));
     static constexpr bool HAS_OBUF = HAS_ST && !DST;  // output tiles leave by TMA store from shared memory
@@ -187,8 +198,14 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         uint64_t* bar = &full[stage];
         unsigned char* sb = stages + stage * Gm::Stage;
         mbar_arrive_expect_tx(bar, Gm::TX);
+#if KS_EVICT_FIRST
+        const uint64_t pol = policy_evict_first();
+        tma_load_3d_hint(sb, in_map, 0, it0 / 32 - (Gm::BASE == kDW ? 0 : 1), irow, bar, pol);
+        if constexpr (Gm::HAS_DW) tma_load_3d_hint(sb + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, irow, bar, pol);
+#else
         tma_load_3d(sb, in_map, 0, it0 / 32 - (Gm::BASE == kDW ? 0 : 1), irow, bar);
         if constexpr (Gm::HAS_DW) tma_load_3d(sb + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, irow, bar);
+#endif
         if constexpr (Gm::BASE >= kFWD) bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * 16, 64, bar);
         it0 += kTT;
         if (it0 >= a.L) {
@@ -251,7 +268,11 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         __syncthreads();
         if (tid == 0) {
             if constexpr (Gm::HAS_OBUF) {
+#if KS_EVICT_FIRST
+                tma_store_3d_hint(out_map, ob, 0, t0 / 32, row, policy_evict_first());
+#else
                 tma_store_3d(out_map, ob, 0, t0 / 32, row);  // columns past L are clipped
+#endif
                 bulk_commit();
             }
             if (u + NS < nunits) issue(stage);
