@@ -42,6 +42,7 @@ struct DwPadGeom {
     int gy_alloc;      // gy rows rounded up to a multiple of 8 (128-byte aligned x box)
     int NBX, nbx;      // x rows per box, x boxes (window = (TT + JT)/32 rows)
     int stage_bytes;   // 1024-aligned
+    int skip;          // skip chunks that read only zero halo (KS_PAD_SKIP=0: compute them)
 };
 
 template <int NJG, bool FUSED>
@@ -124,7 +125,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
             // t + j - p over the warp's chunks and taps.
             const int cb = tu + 32 * (c - ts);
             const int xlo = cb + xw_lo, xhi = cb + xw_hi;
-            if (xhi < 0 || xlo >= L) continue;
+            if (g.skip && (xhi < 0 || xlo >= L)) continue;
             const float* gb = pg + c * 36;         // padded row c of the gy tile
             const float* xb = px + (c + jg) * 36;  // padded row c + jg of the x window
             auto window = [&](const int sub) {
@@ -227,6 +228,10 @@ ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B,
         return KS_OK;
     }
     g.stage_bytes = ((g.gy_alloc + g.nbx * g.NBX) * 144 + 1023) / 1024 * 1024;
+    {
+        const char* e = getenv("KS_PAD_SKIP");
+        g.skip = !(e && *e == '0');
+    }
     int NS = 3;
     while (NS > 2 && dwpad_smem(g, NS) > 110 * 1024) --NS;
     if (const char* e = getenv("KS_DWPAD_NS")) {  // tuning knob

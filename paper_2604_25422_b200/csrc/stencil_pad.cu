@@ -48,6 +48,7 @@ struct PadGeom {
     int Ke;            // taps incl. lead zeros (the live ones)
     int base_row;      // (off + lead) / 32: window origin = t0/32 - base_row
     int off, zlead;    // stencil offset, leading zero taps (tap block jb covers j = 32 jb - zlead ...)
+    int skip;          // drop zero-halo tap blocks (KS_PAD_SKIP=0: compute them)
     int win_floats;    // RPT * nbox * NB * 36
     int stage_bytes;   // window + RPT tap rows, 1024-aligned
 };
@@ -178,8 +179,8 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
         // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
         const int tw = t0 + (lt & ~31) * kR;
-        const int jb_lo = max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64);
-        const int jb_hi = (L + g.off + g.zlead - tw + 31) / 32;
+        const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
+        const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
         float acc[kR];
         if (live)
             tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, jb_lo, jb_hi,
@@ -259,6 +260,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.base_row = static_cast<int>((off + lead) / 32);
     g.off = static_cast<int>(off);
     g.zlead = zlead;
+    g.skip = env_knob("KS_PAD_SKIP", 1) != 0;
     g.RPT = 1;
     while (g.RPT < 8 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
     g.TPR = NT / g.RPT;
