@@ -29,6 +29,33 @@
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
+// Two code-shape choices whose effect depends on how ptxas schedules each
+// instantiation (measured on the B200 with tools/time_paths.py, ABAB):
+//  * warp-uniform row index (lane-0 broadcast): the taps move to uniform
+//    registers, so an FFMA reads two RF operands instead of three -- dX at
+//    K = 128 / 256 (S = 1, producer lane) 4.5% faster, forward (S = 0) 1-1.5%
+//    slower;
+//  * anti-diagonal FFMA order in full windows: forward at K = 4096 (S = 0,
+//    barrier refill) 1% faster, dX there 1-2% slower.
+// Defaults follow those measurements; -DKS_SHFL_RSUB / -DKS_ANTIDIAG = 0 / 1
+// force either everywhere (tools/build_variant.sh).
+template <int S, bool PROD>
+constexpr bool use_shfl() {
+#ifdef KS_SHFL_RSUB
+    return KS_SHFL_RSUB;
+#else
+    return PROD && S == 1;
+#endif
+}
+template <int S, bool PROD>
+constexpr bool use_antidiag() {
+#ifdef KS_ANTIDIAG
+    return KS_ANTIDIAG;
+#else
+    return !PROD && S == 0;
+#endif
+}
+
 namespace ks {
 
 __global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
@@ -58,7 +85,7 @@ struct PadGeom {
 // address pw + pbase (a 32-aligned logical index) and S = 0..3 the sub-quad
 // offset of its first tap.  Each 16-tap register window takes
 // ceil((S + 47) / 4) 128-bit loads (12 for S <= 1, 13 otherwise).
-template <int S, bool FUSED>
+template <int S, bool FUSED, bool ANTID>
 __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pbase, int Ke, int jb_lo, int jb_hi,
                                        float (&acc)[kR]) {
     constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
@@ -83,12 +110,27 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
             w[4 * c + 2] = q.z;
             w[4 * c + 3] = q.w;
         }
+        if (ANTID && nj == kJS) {
+            // anti-diagonal order: the FFMAs sharing window value v[S + m] run
+            // back to back, so it stays in the operand-reuse cache, the tap
+            // comes from a uniform register, and only the accumulator is read
+            // from the register file.  Each acc[r] still sees its taps in
+            // ascending jj = m - r (bit-identical chains).
 #pragma unroll
-        for (int jj = 0; jj < kJS; ++jj)
-            if (jj < nj) {
+            for (int m = 0; m < kR + kJS - 1; ++m)
 #pragma unroll
-                for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[S + r + jj], w[jj]);
-            }
+                for (int r = 0; r < kR; ++r) {
+                    const int jj = m - r;
+                    if (jj >= 0 && jj < kJS) acc[r] = muladd<FUSED>(acc[r], v[S + m], w[jj]);
+                }
+        } else {
+#pragma unroll
+            for (int jj = 0; jj < kJS; ++jj)
+                if (jj < nj) {
+#pragma unroll
+                    for (int r = 0; r < kR; ++r) acc[r] = muladd<FUSED>(acc[r], v[S + r + jj], w[jj]);
+                }
+        }
     };
     // 32-tap blocks [jb_lo, jb_hi) only: the caller drops blocks whose every
     // tap lands in the zero halo for the whole warp (x*0 never changes a chain
@@ -166,7 +208,12 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
             }
     }
 
-    const int rsub = tid / g.TPR, lt = tid - rsub * g.TPR;
+    // a warp lies within one channel row (TPR = 128 / RPT >= 32 since L >= 1024
+    // keeps RPT <= 4); where use_shfl() says so, rsub is broadcast from lane 0
+    // so the compiler can prove the tap addresses warp-uniform and keep the
+    // taps in uniform registers
+    const int rsub = use_shfl<S, PROD>() ? __shfl_sync(0xffffffffu, tid / g.TPR, 0) : tid / g.TPR;
+    const int lt = tid - rsub * g.TPR;
     const int win_rows = g.nbox * g.NB;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
@@ -183,7 +230,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
         float acc[kR];
         if (live)
-            tile32<S, FUSED>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, jb_lo, jb_hi,
+            tile32<S, FUSED, use_antidiag<S, PROD>()>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, jb_lo, jb_hi,
                              acc);
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
@@ -262,7 +309,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.zlead = zlead;
     g.skip = env_knob("KS_PAD_SKIP", 1) != 0;
     g.RPT = 1;
-    while (g.RPT < 8 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
+    while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
     g.TPR = NT / g.RPT;
     const int T = g.TPR * kR;
     g.NR = T / 32 + g.Kp / 32 + (S >= 2 ? 1 : 0);  // S >= 2: 13-quad windows read 4 floats further
