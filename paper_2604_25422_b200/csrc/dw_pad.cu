@@ -25,6 +25,10 @@
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
+#ifndef KS_DWPAD_LANEJG
+#define KS_DWPAD_LANEJG 1  // A/B (tools/build_variant.sh): lanes = tap groups at NJG = 32
+#endif
+
 namespace ks {
 
 namespace {
@@ -64,7 +68,14 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int j0 = g.base + jt * g.JT;
     const int p = K / 2;
     const int tid = threadIdx.x;
-    const int jg = tid / NTS, ts = tid - jg * NTS;
+    // NJG = 32 (K >= 1024): lanes are the 32 tap groups and a warp is one
+    // t-slice, so the gy values of a chunk are warp-uniform (uniform registers,
+    // the FFMA then reads two RF operands; bits unchanged: the same (tap
+    // group, t-slice) work and reduction order, only the thread numbering
+    // moves).  Otherwise a warp spans several t-slices of NJG groups.
+    constexpr bool LANE_JG = NJG == 32 && KS_DWPAD_LANEJG;
+    const int jg = LANE_JG ? (tid & 31) : tid / NTS;
+    const int ts = LANE_JG ? __shfl_sync(0xffffffffu, tid >> 5, 0) : tid - jg * NTS;
     const int ntt = (L + g.TT - 1) / g.TT;
     const int nunits = (b_end - b_begin) * ntt;
     const int xrow_rel = (j0 - p) / 32;  // exact: j0 - p is a multiple of 32
@@ -106,10 +117,10 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 
     const int nchunks = g.TT / 32;
     // this warp's lanes: tap groups [jgw, jgw + JGW) x t-slices [ts_lo, ts_lo + TSW)
-    constexpr int JGW = NTS >= 32 ? 1 : 32 / NTS;
-    constexpr int TSW = NTS >= 32 ? 32 : NTS;
-    const int jgw = (tid & ~31) / NTS;
-    const int ts_lo = NTS >= 32 ? (tid & ~31) % NTS : 0;
+    constexpr int JGW = LANE_JG ? 32 : NTS >= 32 ? 1 : 32 / NTS;
+    constexpr int TSW = LANE_JG ? 1 : NTS >= 32 ? 32 : NTS;
+    const int jgw = LANE_JG ? 0 : (tid & ~31) / NTS;
+    const int ts_lo = LANE_JG ? ts : NTS >= 32 ? (tid & ~31) % NTS : 0;
     const int xw_lo = j0 + 32 * jgw - p + 32 * ts_lo;                         // + t0 of the chunk row
     const int xw_hi = j0 + 32 * (jgw + JGW) - 1 - p + 32 * (ts_lo + TSW) - 1;  // (chunk base i * NTS)
     for (int u = 0; u < nunits; ++u) {
@@ -169,7 +180,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     for (int o = tid; o < g.JT; o += kNT) {
         const int gj = o / kJR, jj = o % kJR;
         float s = 0.f;
-        for (int q = 0; q < NTS; ++q) s += red[(gj * NTS + q) * (kJR + 1) + jj];
+        for (int q = 0; q < NTS; ++q) s += red[(LANE_JG ? q * 32 + gj : gj * NTS + q) * (kJR + 1) + jj];
         const int j = j0 + o;
         if (j >= 0 && j < K) part[(static_cast<int64_t>(grp) * H + h) * K + j] = s;
     }

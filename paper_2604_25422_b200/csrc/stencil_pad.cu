@@ -65,7 +65,6 @@ namespace {
 constexpr int kNT = 128;                     // FMA threads per CTA (one warp per SM sub-partition)
 constexpr int kR = 32;                       // outputs per thread
 constexpr int kJS = 16;                      // taps per register window
-constexpr int kNV = (kR + kJS - 1 + 3) / 4;  // float4 loads per window (12)
 
 struct PadGeom {
     int RPT, TPR;      // channels per tile, threads per channel row (TPR*32 outputs)
