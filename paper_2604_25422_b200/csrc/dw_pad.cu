@@ -25,6 +25,9 @@
 #include "ks_common.cuh"
 #include "ks_tma.cuh"
 
+#ifndef KS_DWPAD_ANTIDIAG
+#define KS_DWPAD_ANTIDIAG 1  // anti-diagonal FFMA order with the uniform-gy mapping (-3.9% at K = 1024 / 4096)
+#endif
 #ifndef KS_DWPAD_LANEJG
 #define KS_DWPAD_LANEJG 1  // A/B (tools/build_variant.sh): lanes = tap groups at NJG = 32
 #endif
@@ -158,10 +161,22 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                     xv[4 * q + 2] = a.z;
                     xv[4 * q + 3] = a.w;
                 }
+                if constexpr (LANE_JG && KS_DWPAD_ANTIDIAG) {
+                    // gy is uniform here: order by x value (m = tt + jj) so it
+                    // stays in the operand-reuse cache; acc[jj] still sees tt ascending
 #pragma unroll
-                for (int tt = 0; tt < kTW; ++tt)
+                    for (int m = 0; m < kTW + kJR - 1; ++m)
 #pragma unroll
-                    for (int jj = 0; jj < kJR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[tt + jj]);
+                        for (int tt = 0; tt < kTW; ++tt) {
+                            const int jj = m - tt;
+                            if (jj >= 0 && jj < kJR) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[m]);
+                        }
+                } else {
+#pragma unroll
+                    for (int tt = 0; tt < kTW; ++tt)
+#pragma unroll
+                        for (int jj = 0; jj < kJR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[tt + jj]);
+                }
             };
             window(0);
             window(16);
