@@ -55,13 +55,9 @@ ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorM
 // but lost at K <= 9 (K = 7: 1.45 -> 1.49 ms), in the fused backward (K = 16:
 // 1.89 -> 2.22 ms) and at config 5a's full size (fwd 11.1 -> 13.4 ms in the
 // bench, ABAB).  KS_DST=1 turns them on (both paths give the same bits).
-inline bool direct_store(const float* out, int64_t K, bool stencil) {
+inline bool direct_store(const float* out) {
     const char* e = getenv("KS_DST");
-    const int knob = e && *e ? atoi(e) : -1;
-    (void)K;
-    (void)stencil;
-    const bool on = knob > 0;
-    return on && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+    return e && atoi(e) > 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 }
 
 inline bool shape_ok(int64_t B, int64_t H, int64_t L, int64_t K) {
@@ -86,7 +82,7 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
     *handled = true;
     const bool f = mode == KS_MULADD_FUSED;
     if constexpr (!DX) return launch_any_k<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, nullptr, st);
-    else return direct_store(dx, K, false) ? launch_any_k<kFUSED | kDirect>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st)
+    else return direct_store(dx) ? launch_any_k<kFUSED | kDirect>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st)
                             : launch_any_k<kFUSED>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st);
 }
 
@@ -108,7 +104,7 @@ inline ks_status launch_stencil_short(const float* in, const float* k, float* ou
     rc = check_launch();
     if (rc == KS_OK) {
         const bool f = mode == KS_MULADD_FUSED;
-        if (direct_store(out, K, true))
+        if (direct_store(out))
             rc = reverse ? launch_any_k<kDXS | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st)
                          : launch_any_k<kFWD | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
         else
