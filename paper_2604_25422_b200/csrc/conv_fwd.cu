@@ -218,6 +218,8 @@ static ks_status launch_direct(const T* in, const T* k, T* out, int64_t B, int64
     return check_launch();
 }
 
+ks_status stencil_ldg_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t, int, int,
+                          cudaStream_t, bool*);
 ks_status stencil_tma_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
                           int, int, cudaStream_t, bool*);
 ks_status stencil_rows_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
@@ -238,6 +240,11 @@ ks_status conv_stencil_f32(const float* in, const float* k, float* out, int64_t 
     if (L < 1024) {  // short rows: whole rows per CTA (rows_short.cu)
         bool handled = false;
         const ks_status s = stencil_rows_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
+        if (handled) return s;
+    }
+    if (!tma_disabled() && K <= 16 && L >= 1024) {  // short kernels: register windows, 256-bit stores
+        bool handled = false;
+        const ks_status s = stencil_ldg_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
         if (handled) return s;
     }
     if (!tma_disabled()) {

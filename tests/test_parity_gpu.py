@@ -322,20 +322,31 @@ def test_bwd_short_equals_generic_kernels(K, monkeypatch):
 
 @pytest.mark.parametrize("K", list(range(1, 17)))
 def test_stencil_short_equals_generic_and_oracle(K, oracle, monkeypatch):
-    """The K-specialised forward / dX stencils (bwd_short.cuh, persistent grid
-    with more rows than CTAs, ragged last tile L = 2080) against the generic
-    stencil_tma they replace (KS_STS=0) bit for bit and, on sampled channels,
-    against the oracle bit for bit, in both multiply-add modes."""
+    """The three short-kernel forward / dX implementations -- register windows
+    with 256-bit stores (stencil_ldg, the default for K <= 8, forced for every
+    K by KS_LDG=2), the K-specialised TMA kernel (bwd_short.cuh, KS_LDG=0;
+    persistent grid with more rows than CTAs) and the generic stencil_tma
+    (KS_LDG=0 KS_STS=0) -- bit for bit against
+    each other and, on sampled channels, against the oracle, in both
+    multiply-add modes, with a ragged last tile (L = 2080)."""
     B, H, L = 40, 16, 2080
     x, k, gy = ks.make_inputs(12, B, H, L, K)
     kh = k.cpu().numpy()
     for m in (SEPARATE, FUSED):
-        monkeypatch.setenv("KS_STS", "0")
-        y_g, dx_g = host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))
-        monkeypatch.delenv("KS_STS")
+        res = []
+        for env in ({"KS_LDG": "2"}, {"KS_LDG": "0"}, {"KS_LDG": "0", "KS_STS": "0"}):
+            for name in ("KS_LDG", "KS_STS"):
+                if name in env:
+                    monkeypatch.setenv(name, env[name])
+                else:
+                    monkeypatch.delenv(name, raising=False)
+            res.append((host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))))
+        for y_o, dx_o in res[1:]:
+            assert same(res[0][0], y_o), m
+            assert same(res[0][1], dx_o), m
+        monkeypatch.delenv("KS_LDG", raising=False)
+        monkeypatch.delenv("KS_STS", raising=False)
         y, dx = ks.forward(x, k, m), ks.backward_input(gy, k, m)
-        assert same(host(y), y_g), m
-        assert same(host(dx), dx_g), m
         for h in (0, H - 1):
             ks_ = np.ascontiguousarray(kh[h:h + 1])
             assert same(_channel_slice(y, h), oracle.forward(_channel_slice(x, h), ks_, m)), (h, m)
@@ -349,6 +360,7 @@ def test_short_kernels_both_output_paths(K, monkeypatch):
     both paths give the same bits (KS_DST=0 / 1 force each)."""
     B, H, L = 40, 16, 4160
     x, k, gy = ks.make_inputs(13, B, H, L, K)
+    monkeypatch.setenv("KS_LDG", "0")  # the stencils through bwd_short, not stencil_ldg
     res = {}
     for d in ("0", "1"):
         monkeypatch.setenv("KS_DST", d)
