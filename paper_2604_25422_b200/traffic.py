@@ -16,8 +16,8 @@ model) extends to B200:
 * ``l2_traffic`` -- modeled L2->SM bytes, which *do* include the halo re-reads
   (TMA boxes overlap by 32*HH floats per side per tile);
 * ``plan(path, B, H, L, K)`` -- which kernel family runs, its tile and grid
-  (mirrors the host dispatch in csrc/: conv_fwd.cu, stencil_tma.cu,
-  bwd_short.cuh, stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
+  (mirrors the host dispatch in csrc/: conv_fwd.cu, stencil_ldg.cu,
+  stencil_tma.cu, bwd_short.cuh, stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
 
 ``tests/test_traffic.py`` checks memory_traffic against the ncu DRAM bytes
 committed in profiles/ncu_summary.json.
@@ -42,6 +42,8 @@ def _stencil_tier(L: int, K: int):
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
     if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
+    if K <= 8 and L >= 1024:
+        return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if K <= 16 and L >= 1024:
         return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
     if L >= 1024:
@@ -106,9 +108,9 @@ def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hie
     base = logical_traffic(path, B, H, L, K)
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
-        kp = 4 * H * (16 if p["kernel"] == "stencil_short" else math.ceil(K / 32) * 32)
+        kp = 4 * H * (16 if p["kernel"] in ("stencil_short", "stencil_ldg") else math.ceil(K / 32) * 32)
         # prep_taps writes kp, the kernel reads it back
-        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short") else 0)
+        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short", "stencil_ldg") else 0)
     if p["kernel"] == "dw_pairwise_tma":
         return base
     return base + 2 * p["partials_bytes"]  # partials written by stage 1, read by stage 2
@@ -121,6 +123,9 @@ def l2_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
     if path not in ("fwd", "dx") or not p["tiles"]:
         return memory_traffic(path, B, H, L, K)
     off = K // 2 if path == "fwd" else K - 1 - K // 2
+    if p["kernel"] == "stencil_ldg":  # window quads past each 2048-output tile (the rest hits L1)
+        halo = p["tiles"] * 2 * 4 * math.ceil((max(off, K - 1 - off) + 3) / 4) * 4
+        return memory_traffic(path, B, H, L, K) + halo
     HH = 1 if p["kernel"] == "stencil_short" else max(1, math.ceil(max(off, K - 1 - off) / 32))
     halo = p["tiles"] * 2 * 32 * HH * 4
     return memory_traffic(path, B, H, L, K) + halo
