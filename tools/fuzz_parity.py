@@ -5,7 +5,8 @@ For N random shapes (B, H, L, K) -- L drawn to hit every dispatch tier
 (short rows, L % 8 / % 32 / ragged, long rows) and K from 1 to 600 -- checks
 fwd / dX bitwise against the oracle on sampled channels in both multiply-add
 modes, dW HIERARCHICAL against the fp64 oracle to the parity tolerance, and
-the fused backward bitwise against the separate calls.  Prints one line per
+the fused backward bitwise against the separate calls; for small reductions
+also the reference's SEQUENTIAL / PAIRWISE / CHUNKED(c) dW bit for bit.  Prints one line per
 failure and a summary.
 
 usage: python tools/fuzz_parity.py [--n 200] [--seed 0]
@@ -21,7 +22,7 @@ import torch
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import paper_2604_25422_b200 as ks  # noqa: E402
-from oracle.oracle import FUSED, SEPARATE, SEQUENTIAL, Oracle, normwise  # noqa: E402
+from oracle.oracle import CHUNKED, FUSED, PAIRWISE, SEPARATE, SEQUENTIAL, Oracle, normwise  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--n", type=int, default=200)
@@ -70,6 +71,17 @@ for it in range(a.n):
         err = normwise(dk[h:h + 1].cpu().numpy(), truth)
         if not err <= 1e-4:
             bad.append(f"dW h={h} normwise {err:.2e}")
+    # the reference's own association orders, bit for bit (small reductions only)
+    if B * L <= 40000:
+        h = hs[-1]
+        xs = np.ascontiguousarray(x[:, h:h + 1].cpu().numpy())
+        gs = np.ascontiguousarray(gy[:, h:h + 1].cpu().numpy())
+        for sch, c in ((SEQUENTIAL, 0), (PAIRWISE, 0), (CHUNKED, rng.randint(1, 3000))):
+            for m in (SEPARATE, FUSED):
+                got = ks.backward_weight(gy, x, K, sch, c, m)[h:h + 1].cpu().numpy()
+                ref = o.backward_weight(gs, xs, K, sch, c, m)
+                if not np.array_equal(got.view(np.uint32), ref.view(np.uint32)):
+                    bad.append(f"dW scheme={sch} chunk={c} m={m} h={h} not bitwise")
     if bad:
         fails += 1
         print(f"FAIL ({B},{H},{L},{K}) tier={tier}: {'; '.join(bad)}", flush=True)
