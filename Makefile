@@ -19,8 +19,8 @@ REF_ROOT ?= /root/reference/proj
 NVFLAGS  := $(ARCH) -O3 -lineinfo -std=c++20 -Xcompiler -fPIC -Iinclude -I$(CSRC) \
             --expt-relaxed-constexpr -Xptxas -v -Xcompiler -Wall
 CU_SRCS  := $(CSRC)/capi.cu $(CSRC)/conv_fwd.cu $(CSRC)/conv_dw.cu $(CSRC)/conv_tma.cu \
-            $(CSRC)/stencil_tma.cu $(CSRC)/dw_tma.cu $(CSRC)/bwd_short_dw.cu $(CSRC)/bwd_short_dx.cu $(CSRC)/bwd_short_st.cu $(CSRC)/stencil_ldg.cu $(CSRC)/dw_pairwise_tma.cu $(CSRC)/paper_variants.cu $(CSRC)/stencil_cb.cu $(CSRC)/stencil_pad.cu $(CSRC)/rows_short.cu $(CSRC)/dw_cb.cu $(CSRC)/dw_pad.cu \
-            $(CSRC)/host_api.cu $(CSRC)/dist.cu $(CSRC)/peer.cu
+            $(CSRC)/stencil_tma.cu $(CSRC)/dw_tma.cu $(CSRC)/bwd_short_dw.cu $(CSRC)/bwd_short_dx.cu $(CSRC)/bwd_short_st.cu $(CSRC)/stencil_ldg.cu $(CSRC)/dw_pairwise_tma.cu $(CSRC)/paper_variants.cu $(CSRC)/stencil_pad.cu $(CSRC)/rows_short.cu $(CSRC)/dw_pad.cu \
+            $(CSRC)/host_api.cu $(CSRC)/dist.cu $(CSRC)/peer.cu $(CSRC)/options.cu
 CPP_SRCS := $(CSRC)/conv_core.cpp
 OBJDIR   := build/obj
 CU_OBJS  := $(patsubst $(CSRC)/%.cu,$(OBJDIR)/%.o,$(CU_SRCS))

@@ -4,24 +4,33 @@
 Metric (BASELINE.json): effective HBM GB/s and % of the HBM roofline per path
 (fwd / dX / dW), and fwd+bwd conv time per step.
 
-* A "step" is one pass of the hot path over one batch: y = forward(x,k),
-  dx = backward_input(gy,k), dk = backward_weight(gy,x) (+ the dW combine over
-  ranks when N > 1), all through the library's C ABI on resident device
-  buffers.  Inputs come from the reference's splitmix64 stream generated in
-  place on the device.
+* A "step" is one pass of the hot path over one batch: y = forward(x,k), then
+  the layer's backward dx = backward_input(gy,k), dk = backward_weight(gy,x)
+  (+ the dW combine over ranks when N > 1), all through the library's C ABI
+  on resident device buffers.  Inputs come from the reference's splitmix64
+  stream generated in place on the device.
 * Default workload: BASELINE config 3 (B=256, H=512, L=8192, K=7, fp32), the
   largest single-GPU config and the one the north star's roofline targets are
   stated on.  4 GiB per tensor >> 126 MB L2, so no L2 flush is needed.
-* value = algorithmic bytes of the three paths (8*B*H*L + 4*H*K each,
-  reference src/exec_model.cpp:168-179) over all ranks / device step time
-  (CUDA events, max over ranks).  Weak scaling: every rank runs the per-GPU
-  batch B, the global batch is B*N, sharded by contiguous batch rows.
-* e2e: the same metric through the host-buffer C-ABI entry points
-  (ks_dwconv1d_*_host, the reference's value-type API shape) from pinned host
-  memory, H2D/D2H inside the timed region.
+  Default multiply-add mode: Separate, the reference's default
+  (conv_core.hpp:50,57) -- both arms compute bit-identical y / dX.
+* value = the step's compulsory HBM bytes over all ranks / device step time
+  (CUDA events, max over ranks).  Compulsory bytes of one step: forward reads
+  x and k and writes y; the backward reads gy, x and k and writes dx and dk:
+  20*B*H*L + 12*H*K.  (The per-path table keeps the reference's per-path
+  logical bytes, 8*B*H*L + 4*H*K each, src/exec_model.cpp:168-179.)  The
+  reference arm divides the same bytes by its own time, so the two values'
+  ratio is the time ratio.
+* Scaling: weak by default (every rank runs the config's batch, global batch
+  B*N); --global-batch G fixes the global batch and shards it with
+  ks_shard_rows (strong scaling, BASELINE configs 4 and 5).
+* e2e: the same metric end to end from pinned host memory, H2D/D2H inside the
+  timed region, through the drop-in's three host calls (forward,
+  backward_input, backward_weight: the reference's value-type API); the
+  library's one-call ks_dwconv1d_step_f32_host is reported beside it.
 * --impl reference: the reference's own CPU conv_core.cpp (oracle/_ref, built
   from /root/reference) on the host cores, channel-sliced over threads, on a
-  bounded channel sample of the same workload.
+  bounded channel sample of the same workload, in the same mode.
 """
 from __future__ import annotations
 
@@ -66,6 +75,12 @@ def path_bytes(B, H, L, K):
     return 8 * B * H * L + 4 * H * K
 
 
+def step_bytes(B, H, L, K):
+    """Compulsory HBM bytes of one training step of the layer: forward reads x,
+    k and writes y; the backward reads gy, x, k and writes dx, dk."""
+    return 20 * B * H * L + 12 * H * K
+
+
 def path_flops(B, H, L, K):
     return 2 * B * H * L * K  # reference src/analyzer.cpp:36-49
 
@@ -74,11 +89,22 @@ def useful_flops(B, H, L, K):
     """2 x the taps that touch the row: the paper's count includes
     taps on the zero padding, 25% of them at K = L.  Same total for fwd (sum over
     t of the valid j), dX and dW (sum over j of the valid t)."""
-    import numpy as np
     p = K // 2
     t = np.arange(L, dtype=np.int64)
     n = np.clip(np.minimum(K, L + p - t) - np.maximum(0, p - t), 0, None).sum()
     return 2 * B * H * int(n)
+
+
+def bench_config(cfg_name, args, world):
+    """The `config` dict -- identical in both arms (the driver compares them)."""
+    B, H, L, K = CONFIGS[cfg_name]
+    strong = bool(args.global_batch)
+    gb = args.global_batch if strong else B * world
+    return {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B": gb, "H": H, "L": L, "K": K,
+            "global_batch": gb, "B_per_gpu": (-(-gb // world) if strong else B), "n_gpus": world,
+            "scaling": "strong" if strong else "weak", "mode": args.mode, "dw_scheme": args.scheme,
+            "bytes_per_step": step_bytes(gb, H, L, K),
+            "value_def": "compulsory HBM bytes of the step (20*B*H*L + 12*H*K) / step time"}
 
 
 def measured_peaks():
@@ -195,23 +221,36 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 # CPU legs (oracle/_ref = the reference's own conv_core.cpp)
 
-def cpu_sample(cfg, threads, budget_s=12.0, mode=1, reps=1):
-    """Time fwd + dX + dW (reference default dW scheme: sequential) of the
-    reference CPU implementation on a channel sample of the workload, fanned
-    out over `threads` host threads.  Returns (GB/s, seconds, sample dict)."""
-    from oracle.oracle import SEQUENTIAL, Reference, reference_available, Oracle
-    B, H, L, K = cfg
+def _ref_impl():
+    from oracle.oracle import Oracle, Reference, reference_available
     impl = Reference() if reference_available() else Oracle()
-    kind = "reference" if isinstance(impl, Reference) else "port"
+    return impl, ("reference" if isinstance(impl, Reference) else "port")
+
+
+def _ref_step(impl, x, k, gy, K, mode, threads):
+    """One step of the reference CPU implementation (default dW scheme
+    Sequential, src/conv_core.cpp:98-111) on a channel slice."""
+    from oracle.oracle import SEQUENTIAL
+    t0 = time.perf_counter()
+    impl.forward(x, k, mode, threads=threads)
+    impl.backward_input(gy, k, mode, threads=threads)
+    impl.backward_weight(gy, x, K, SEQUENTIAL, 0, mode, threads=threads)
+    return time.perf_counter() - t0
+
+
+def cpu_sample(cfg, threads, mode, budget_s=12.0):
+    """Time fwd + dX + dW of the reference CPU implementation on a channel
+    sample of the workload (all B rows), fanned out over `threads` host
+    threads.  Returns (GB/s of the step's compulsory bytes, full-step seconds
+    extrapolated to all H channels, sample text, kind)."""
+    from oracle.oracle import Oracle
+    B, H, L, K = cfg
+    impl, kind = _ref_impl()
+    o = Oracle()
 
     def run(hs):
-        o = Oracle()
         x, k, gy = o.fill_inputs(7, B, hs, L, K)
-        t0 = time.perf_counter()
-        impl.forward(x, k, mode, threads=threads)
-        impl.backward_input(gy, k, mode, threads=threads)
-        impl.backward_weight(gy, x, K, SEQUENTIAL, 0, mode, threads=threads)
-        return time.perf_counter() - t0
+        return _ref_step(impl, x, k, gy, K, mode, threads)
 
     hs = min(H, max(1, threads))
     t = run(hs)
@@ -221,53 +260,61 @@ def cpu_sample(cfg, threads, budget_s=12.0, mode=1, reps=1):
     if t < budget_s / 2 and hs < H:
         hs = min(H, max(hs, int(hs * (budget_s / 2) / max(t, 1e-3))))
         t = run(hs)
-    times = [t] + [run(hs) for _ in range(reps - 1)]
-    t = min(times)
-    bytes_ = 3 * path_bytes(B, hs, L, K)
+    mname = "Separate" if mode == 0 else "Fused"
     sample = (f"{hs} of {H} channels (all B={B} rows, L={L}, K={K}), fwd+dX+dW(sequential), "
-              f"{threads} threads channel-sliced, {kind} build; full-step time extrapolated x{H / hs:.1f}")
-    return bytes_ / t / 1e9, t * H / hs, sample, kind
+              f"MulAddMode::{mname}, {threads} threads channel-sliced, {kind} build; full-step time "
+              f"extrapolated x{H / hs:.1f}")
+    return step_bytes(B, hs, L, K) / t / 1e9, t * H / hs, sample, kind
 
 
 def run_reference(args, cfg_name, cfg):
+    """The reference arm: the reference's own conv_core.cpp on the host cores,
+    the same config dict, metric and bytes as this repo's arm."""
     rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return 0
     threads = os.cpu_count() or 1
     B, H, L, K = cfg
-    from oracle.oracle import SEQUENTIAL, Reference, reference_available, Oracle
-    impl = Reference() if reference_available() else Oracle()
-    kind = "reference" if isinstance(impl, Reference) else "port"
-    # size the per-step channel sample so warmup+steps fit in ~2 minutes
-    _, full_s, _, _ = cpu_sample(cfg, threads, budget_s=4.0)
+    mode = 1 if args.mode == "fused" else 0
+    impl, kind = _ref_impl()
+    from oracle.oracle import Oracle
+    # size the per-step channel sample so warmup + steps fit in ~2 minutes
+    _, full_s, _, _ = cpu_sample(cfg, threads, mode, budget_s=4.0)
     per_channel = full_s / H
     total_steps = args.steps + args.warmup
-    hs = int(max(1, min(H, 110.0 / total_steps / max(per_channel, 1e-6))))
-    o = Oracle()
-    x, k, gy = o.fill_inputs(7, B, hs, L, K)
+    hs = int(max(1, min(H, 100.0 / total_steps / max(per_channel, 1e-6))))
+    x, k, gy = Oracle().fill_inputs(7, B, hs, L, K)
     times = []
     for i in range(total_steps):
-        t0 = time.perf_counter()
-        impl.forward(x, k, 1, threads=threads)
-        impl.backward_input(gy, k, 1, threads=threads)
-        impl.backward_weight(gy, x, K, SEQUENTIAL, 0, 1, threads=threads)
+        t = _ref_step(impl, x, k, gy, K, mode, threads)
         if i >= args.warmup:
-            times.append(time.perf_counter() - t0)
+            times.append(t)
     t = sum(times) / len(times)
-    gbs = 3 * path_bytes(B, hs, L, K) / t / 1e9
-    sample = (f"{hs} of {H} channels per step (all B={B} rows), fwd+dX+dW(sequential, Fused), "
-              f"{threads} threads channel-sliced")
+    gbs = step_bytes(B, hs, L, K) / t / 1e9
+    # side number: the other MulAddMode (Fused is a libm fma call in the
+    # reference's Release build, ~2.5-3x slower than Separate)
+    other = 1 - mode
+    t_other = _ref_step(impl, x, k, gy, K, other, threads)
+    mname = "Separate" if mode == 0 else "Fused"
+    sample = (f"{hs} of {H} channels per step (all B={B} rows), fwd+dX+dW(sequential), MulAddMode::{mname}, "
+              f"{threads} threads channel-sliced, {kind} build")
+    conf = bench_config(cfg_name, args, world)
+    gb = conf["global_batch"]
     line = {
         "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": round(t * H / hs * 1e3, 3), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B": B, "H": H, "L": L,
-                   "K": K, "global_batch": B, "ms_per_step_note": "extrapolated to all H channels"},
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(t * H / hs * gb / B * 1e3, 3), "higher_is_better": True,
+        "scaling": conf["scaling"], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": conf,
+        "ms_per_step_note": f"extrapolated from {hs} of {H} channels and {B} rows to the whole global batch",
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
                          "sample": sample},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "side": {"mode": "fused" if other else "separate",
+                 "value": round(step_bytes(B, hs, L, K) / t_other / 1e9, 4), "unit": "GB/s",
+                 "note": "one step of the same sample in the other MulAddMode"},
     }
     print(json.dumps(line), flush=True)
     return 0
@@ -285,15 +332,20 @@ def run_ours(args, cfg_name, cfg):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if world != args.gpus:
-        if world == 1 and args.gpus > 1:
-            print("bench.py: --gpus N>1 must be launched under torchrun", file=sys.stderr)
-            return 2
+    if world != args.gpus and world == 1 and args.gpus > 1:
+        print("bench.py: --gpus N>1 must be launched under torchrun", file=sys.stderr)
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    B, H, L, K = cfg
+    Bc, H, L, K = cfg
+    conf = bench_config(cfg_name, args, world)
+    B_total = conf["global_batch"]
+    if args.global_batch:  # strong scaling: this rank's contiguous rows of the global batch
+        b0, B = ks.shard_rows(B_total, world, rank)
+    else:  # weak scaling: every rank the config's batch
+        b0, B = rank * Bc, Bc
     mode = ks.FUSED if args.mode == "fused" else ks.SEPARATE
     scheme = {"hierarchical": ks.HIERARCHICAL, "pairwise": ks.PAIRWISE}[args.scheme]
 
@@ -303,15 +355,14 @@ def run_ours(args, cfg_name, cfg):
         dist.broadcast_object_list(uid, src=0)
         comm = ks.Comm(uid[0], world, rank)
         if args.combine == "peer" and scheme == ks.HIERARCHICAL:
-            peer = comm.peer(B, H, L, K)  # NVLink peer-memory combine fused into dW
+            # NVLink peer-memory combine fused into dW (global plan: = the 1-GPU bits when shards align)
+            peer = comm.peer(B, H, L, K, B_total=B_total)
 
-    # inputs: rows [rank*B, rank*B+B) of the (B*world)-row problem, generated in place
-    x, k, gy = ks.make_inputs(args.seed, B, H, L, K, device=dev, b0=rank * B, B_total=B * world)
+    x, k, gy = ks.make_inputs(args.seed, B, H, L, K, device=dev, b0=b0, B_total=B_total)
     y = torch.empty_like(x)
     dx = torch.empty_like(gy)
     dk = torch.empty((H, K), dtype=torch.float32, device=dev)
-    ws = torch.empty(max(1, ks.workspace_bytes(B, H, L, K, scheme) // 4), dtype=torch.float32,
-                     device=dev)
+    ws = torch.empty(max(1, ks.workspace_bytes(B, H, L, K, scheme) // 4), dtype=torch.float32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     def run_fwd():
@@ -322,55 +373,54 @@ def run_ours(args, cfg_name, cfg):
 
     def run_dw():
         if peer is not None:  # stage 1 + fused signal/wait/combine over peer memory
-            peer.backward_weight(gy, x, K, mode, out=dk)
+            peer.backward_weight(gy, x, K, mode, out=dk, B_total=B_total)
         else:
             ks.backward_weight(gy, x, K, scheme, 0, mode, out=dk, workspace=ws)
 
-    paths_fn = [run_fwd, run_dx, run_dw]
+    def run_bwd():
+        ks.backward(gy, x, k, mode, out=(dx, dk), workspace=ws)
 
-    def step(ev=None):
-        for i, fn in enumerate(paths_fn):
-            if ev:
-                ev[i].record(stream)
-            fn()
-        if ev:
-            ev[3].record(stream)
-        if comm is not None and peer is None:
-            comm.allreduce_dw(dk)
-        if ev:
-            ev[4].record(stream)
+    fused_bwd = args.bwd == "fused" and peer is None and scheme == ks.HIERARCHICAL
+    # split step (gives the per-path table) and the step proper (forward, then
+    # the layer's backward in ONE call where it fuses): each path's launches
+    # are captured once into a CUDA graph and replayed, so the timed region
+    # holds device work only.  The NCCL / peer dW combine stays eager.
+    split_fns = [run_fwd, run_dx, run_dw]
+    step_fns = [run_fwd, run_bwd] if fused_bwd else list(split_fns)
+    launches = {}  # launches of our kernels per call of each path
 
-    # the clock sampler (an nvidia-smi child) starts before the warm-up so its
-    # process start-up cannot stall the host inside the timed region
+    def count(fn):
+        c0 = ks.launch_count()
+        fn()
+        return ks.launch_count() - c0
+
     clk = ClockSampler(local).__enter__()
     for _ in range(args.warmup):
-        step()
+        for fn in split_fns + step_fns[1:]:
+            fn()
     torch.cuda.synchronize()
-    # each path's launches (tap staging, kernel(s), stream-ordered scratch) are
-    # captured once into a CUDA graph and replayed: the timed region then holds
-    # device work only, not the host's per-call launch overhead (which decides
-    # launch-bound configs such as config 1).  The NCCL dW combine stays eager.
-    graphs = None
-    if not args.no_graphs and peer is None:
+    use_graphs = not args.no_graphs and peer is None
+    graphs = {}
+    if use_graphs:
         try:
-            graphs = []
-            for fn in paths_fn:
+            for fn in set(split_fns + step_fns):
                 g = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(g):
-                    fn()
-                graphs.append(g)
+                    launches[fn] = count(fn)
+                graphs[fn] = g
         except Exception as exc:  # capture unsupported here: stay eager, say so
             print(f"bench.py: CUDA graph capture failed ({exc}); timing eager launches", file=sys.stderr)
-            graphs = None
+            graphs = {}
             torch.cuda.synchronize()
-        if graphs is not None:
-            paths_fn = [g.replay for g in graphs]
-        for _ in range(args.warmup):
-            step()
-        torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    if not graphs:
+        for fn in set(split_fns + step_fns):
+            launches[fn] = count(fn)
     torch.cuda.synchronize()
+    play = {fn: (graphs[fn].replay if fn in graphs else fn) for fn in set(split_fns + step_fns)}
+
+    def combine():
+        if comm is not None and peer is None:
+            comm.allreduce_dw(dk)
 
     # working sets that fit in L2 (126 MB; configs 1 and 2) get L2 flushed
     # before every timed step by writing a 512 MB buffer, outside the timed
@@ -378,137 +428,106 @@ def run_ours(args, cfg_name, cfg):
     flush = None
     if 4 * B * H * L * 2 < 4 * 126e6:
         flush = torch.empty(128 << 20, dtype=torch.float32, device=dev)
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
-    start = torch.cuda.Event(enable_timing=True)
-    end = torch.cuda.Event(enable_timing=True)
-    start.record(stream)
-    for i in range(args.steps):
-        if flush is not None:
-            flush.fill_(float(i))
-        step(evs[i])
-    end.record(stream)
-    torch.cuda.synchronize()
 
-    # The step proper: forward, then the layer's backward in ONE call
-    # (ks_dwconv1d_bwd_f32: dX and dW from a single pass over gy and x where
-    # the fused kernel applies, bitwise the same dx / dk as the split calls
-    # timed above, which give the per-path table).
-    fused_bwd = args.bwd == "fused" and peer is None and scheme == ks.HIERARCHICAL
-    fevs = None
-    if fused_bwd:
-        def run_bwd():
-            ks.backward(gy, x, k, mode, out=(dx, dk), workspace=ws)
-
-        bwd_fn = run_bwd
-        if graphs is not None:
-            gb = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(gb):
-                run_bwd()
-            graphs.append(gb)
-            bwd_fn = gb.replay
-
-        def fstep(ev=None):
-            if ev:
-                ev[0].record(stream)
-            paths_fn[0]()
-            if ev:
-                ev[1].record(stream)
-            bwd_fn()
-            if ev:
-                ev[2].record(stream)
-            if comm is not None:
-                comm.allreduce_dw(dk)
-            if ev:
-                ev[3].record(stream)
-
+    def timed(fns, with_combine):
+        """Times args.steps steps of fns (+ combine): per-step event splits and
+        the whole-loop time (flushes excluded)."""
         for _ in range(args.warmup):
-            fstep()
+            for fn in fns:
+                play[fn]()
+            combine()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        fevs = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
-        fstart = torch.cuda.Event(enable_timing=True)
-        fend = torch.cuda.Event(enable_timing=True)
-        fstart.record(stream)
+        n = len(fns) + 2
+        evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n)] for _ in range(args.steps)]
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
         for i in range(args.steps):
             if flush is not None:
                 flush.fill_(float(i))
-            fstep(fevs[i])
-        fend.record(stream)
+            for j, fn in enumerate(fns):
+                evs[i][j].record(stream)
+                play[fn]()
+            evs[i][len(fns)].record(stream)
+            if with_combine:
+                combine()
+            evs[i][len(fns) + 1].record(stream)
+        end.record(stream)
         torch.cuda.synchronize()
+        per = np.array([[e[j].elapsed_time(e[j + 1]) for j in range(n - 1)] for e in evs])
+        total = start.elapsed_time(end) if flush is None else float(sum(e[0].elapsed_time(e[-1]) for e in evs))
+        return per, total
+
+    per_split, ms_split_total = timed(split_fns, True)
+    per_step, ms_total = (per_split, ms_split_total) if not fused_bwd else timed(step_fns, True)
     clk.__exit__(None, None, None)
+    split_mean = per_split.mean(axis=0)  # fwd, dX, dW, combine
+    step_mean = per_step.mean(axis=0)    # fwd, bwd (or dX, dW), combine
     if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    per = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(4)] for e in evs])  # steps x 4
-    per_mean = per.mean(axis=0)
-    # the step is first path start -> combine end, summed over steps (flushes excluded)
-    ms_total = start.elapsed_time(end) if flush is None else float(
-        sum(e[0].elapsed_time(e[4]) for e in evs))
-    fper_mean = np.zeros(3)
-    if fused_bwd:
-        fper_mean = np.array([[e[i].elapsed_time(e[i + 1]) for i in range(3)] for e in fevs]).mean(axis=0)
-        ms_total = fstart.elapsed_time(fend) if flush is None else float(
-            sum(e[0].elapsed_time(e[3]) for e in fevs))
-    if world > 1:
-        t = torch.tensor([ms_total] + per_mean.tolist() + fper_mean.tolist(), dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total] + split_mean.tolist() + step_mean.tolist(), dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_total, per_mean, fper_mean = float(t[0]), t[1:5].cpu().numpy(), t[5:8].cpu().numpy()
+        v = t.cpu().numpy()
+        ms_total, split_mean, step_mean = float(v[0]), v[1:1 + len(split_mean)], v[1 + len(split_mean):]
     ms_step = ms_total / args.steps
 
     if args.timing_log and rank == 0:
         # the reference's timing-log schema (src/timing_log.cpp:44-97): one row
         # per path per timed step; conv_total = fwd + bwd_in + bwd_k (PAPER.md:563)
         with open(args.timing_log, "w") as f:
-            f.write("# kernelscope timing log from the B200 library (bench.py); variant b200_tma\n")
+            f.write(f"# kernelscope timing log from the B200 library (bench.py), {cfg_name}; "
+                    f"variant {args.timing_variant}\n")
             f.write("variant,path,runtime_ms,run_id\n")
-            for i, row in enumerate(per):
+            for i, row in enumerate(per_split):
                 for name, v in zip(("fwd", "bwd_in", "bwd_k"), row[:3]):
-                    f.write(f"b200_tma,{name},{v:.6f},{i}\n")
-                f.write(f"b200_tma,conv_total,{float(sum(row[:3])):.6f},{i}\n")
+                    f.write(f"{args.timing_variant},{name},{v:.6f},{i}\n")
+                f.write(f"{args.timing_variant},conv_total,{float(sum(row[:3])):.6f},{i}\n")
 
     pb = path_bytes(B, H, L, K)
-    value = world * 3 * pb / (ms_step * 1e-3) / 1e9
+    value = step_bytes(B_total, H, L, K) / (ms_step * 1e-3) / 1e9
     peak, peak_kind = measured_peaks()
     names = ["fwd", "dX", "dW"]
     paths = {}
     for i, n in enumerate(names):
-        gbs = pb / (per_mean[i] * 1e-3) / 1e9
-        fl = path_flops(B, H, L, K) / (per_mean[i] * 1e-3) / 1e12
-        ufl = useful_flops(B, H, L, K) / (per_mean[i] * 1e-3) / 1e12
-        paths[n] = {"ms": round(float(per_mean[i]), 4), "GB_s": round(gbs, 1),
+        gbs = pb / (split_mean[i] * 1e-3) / 1e9
+        fl = path_flops(B, H, L, K) / (split_mean[i] * 1e-3) / 1e12
+        ufl = useful_flops(B, H, L, K) / (split_mean[i] * 1e-3) / 1e12
+        paths[n] = {"ms": round(float(split_mean[i]), 4), "GB_s": round(gbs, 1),
                     "frac_hbm_measured": round(gbs / peak, 4), "frac_hbm_8TBs": round(gbs / 8000, 4),
                     "TFLOP_s_paper": round(fl, 2), "TFLOP_s_useful": round(ufl, 2)}
     if world > 1:
-        paths["dW_allreduce"] = {"ms": round(float(per_mean[3]), 4), "bytes": 4 * H * K}
+        comb_ms = float(step_mean[-1]) if peer is None else None
+        paths["dW_combine"] = {"ms": None if comb_ms is None else round(comb_ms, 4), "bytes": 4 * H * K,
+                               "kind": "peer-memory (fused into dW)" if peer is not None else "ncclAllReduce",
+                               "share_of_step": None if comb_ms is None else round(comb_ms / ms_step, 4)}
+    fused_kernel = fused_bwd and L % 32 == 0 and L >= 2048 and K <= 16
     if fused_bwd:
         # logical bytes of the two paths it replaces vs the bytes it moves
         # (fused kernel: read gy + x, write dx = 12 B per element; else 16)
-        fused_kernel = L % 32 == 0 and L >= 2048 and K <= 16
         moved = (12 if fused_kernel else 16) * B * H * L + 8 * H * K
-        paths["bwd_fused"] = {"ms": round(float(fper_mean[1]), 4),
-                              "GB_s_logical": round(2 * pb / (fper_mean[1] * 1e-3) / 1e9, 1),
+        paths["bwd_fused"] = {"ms": round(float(step_mean[1]), 4),
+                              "GB_s_logical": round(2 * pb / (step_mean[1] * 1e-3) / 1e9, 1),
                               "bytes_moved": moved,
-                              "GB_s_moved": round(moved / (fper_mean[1] * 1e-3) / 1e9, 1),
-                              "frac_hbm_measured": round(moved / (fper_mean[1] * 1e-3) / 1e9 / peak, 4),
+                              "GB_s_moved": round(moved / (step_mean[1] * 1e-3) / 1e9, 1),
+                              "frac_hbm_measured": round(moved / (step_mean[1] * 1e-3) / 1e9 / peak, 4),
                               "fused_kernel": fused_kernel}
-    dom = int(np.argmax(per_mean[:3]))
+    dom = int(np.argmax(split_mean[:3]))
     traffic = ncu_traffic(cfg_name)
     dom_traffic = None
     if traffic and names[dom] in traffic:
         dom_traffic = traffic[names[dom]].get("dram_bytes")
-    achieved = pb / (per_mean[dom] * 1e-3) / 1e9
+    achieved = pb / (split_mean[dom] * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": dom_traffic,
                 "kernel": names[dom], "peak_kind": peak_kind,
                 "algorithmic_bytes_per_launch": pb,
                 "note": "achieved = (8*B*H*L + 4*H*K) bytes / mean CUDA-event duration of the path"}
-    if fused_bwd and paths["bwd_fused"]["fused_kernel"] and fper_mean[1] > fper_mean[0]:
+    if fused_kernel and step_mean[1] > step_mean[0]:
         # the step's dominant kernel is the fused backward: its algorithmic
         # (compulsory) bytes are read gy + x, write dx, read k, write dk
         fb = paths["bwd_fused"]["bytes_moved"]
-        ach = fb / (fper_mean[1] * 1e-3) / 1e9
+        ach = fb / (step_mean[1] * 1e-3) / 1e9
         bt = traffic.get("bwd", {}).get("dram_bytes") if traffic else None
         roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": peak, "unit": "GB/s",
                     "frac": round(ach / peak, 4), "traffic": bt, "kernel": "bwd_fused (dX + dW, one pass)",
@@ -517,21 +536,21 @@ def run_ours(args, cfg_name, cfg):
                             "per-path split numbers in `paths`"}
     # long K is FP32-FMA-bound (paper arithmetic intensity K/4 FLOP/B above the
     # ridge): report against the FP32 roof measured in-process instead
-    fp32 = C_double = None
+    fp32 = None
     if K / 4.0 > 12.0:
         import ctypes
-        C_double = ctypes.c_double(0.0)
-        if ks.lib().ks_probe_fp32_tflops(ctypes.byref(C_double)) == 0:
-            fp32 = C_double.value
+        c = ctypes.c_double(0.0)
+        if ks.lib().ks_probe_fp32_tflops(ctypes.byref(c)) == 0:
+            fp32 = c.value
     if fp32:
         fl = path_flops(B, H, L, K)
         ufl = useful_flops(B, H, L, K)
-        ach = ufl / (per_mean[dom] * 1e-3) / 1e12
+        ach = ufl / (split_mean[dom] * 1e-3) / 1e12
         roofline = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32, 2), "unit": "TFLOP/s",
                     "frac": round(ach / fp32, 4), "traffic": dom_traffic, "kernel": names[dom],
                     "peak_kind": "measured in-process (ks_probe_fp32_tflops: FFMA loop on all SMs)",
                     "algorithmic_flops_per_launch": ufl, "paper_flops_per_launch": fl,
-                    "frac_paper_flops": round(fl / (per_mean[dom] * 1e-3) / 1e12 / fp32, 4),
+                    "frac_paper_flops": round(fl / (split_mean[dom] * 1e-3) / 1e12 / fp32, 4),
                     "note": "compute-bound (K/4 FLOP/B > ridge); achieved = useful FLOPs (2 x taps that touch "
                             "the row, SURVEY 8(d)) / mean CUDA-event duration of the path; the paper's "
                             "2*B*H*L*K also counts taps on the zero padding (frac_paper_flops); HBM GB/s "
@@ -539,17 +558,13 @@ def run_ours(args, cfg_name, cfg):
         for n in names:
             paths[n]["frac_fp32_measured"] = round(paths[n]["TFLOP_s_useful"] / fp32, 4)
             paths[n]["frac_fp32_paper_flops"] = round(paths[n]["TFLOP_s_paper"] / fp32, 4)
-    # our kernels per step: fwd and dX = prep_taps + stencil_tma each (TMA path,
-    # L % 32 == 0) or one conv_tile_f32; dW = stage 1 + the fixed-order
-    # cross-block pass (hierarchical and pairwise alike)
-    launches_per_step = (2 * 2 if L % 32 == 0 else 2) + 2
-    launches = launches_per_step * args.steps
-    if fused_bwd:  # the fused-step loop: fwd (2) + bwd (fused kernel + group sum, or the split 4)
-        fused_kernel = L % 32 == 0 and L >= 2048 and K <= 16
-        launches += ((2 if L % 32 == 0 else 1) + (2 if fused_kernel else launches_per_step - 2)) * args.steps
+    # our kernels launched inside the two timed loops (counted by the library
+    # at capture / launch time: ks_launch_count)
+    gpu_launches = args.steps * (sum(launches[f] for f in split_fns) +
+                                 (sum(launches[f] for f in step_fns) if fused_bwd else 0))
 
-    # ---- end to end through the host-buffer C ABI (pinned host memory) ----
-    e2e = None
+    # ---- end to end from pinned host memory (H2D / D2H inside the timed region) ----
+    e2e = e2e_step = None
     e2e_note = None
     if not args.no_e2e:
         # every rank pins x, gy, y, dx on the same host: skip (and say so) when
@@ -576,75 +591,78 @@ def run_ours(args, cfg_name, cfg):
         del y, dx
         torch.cuda.empty_cache()
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
-
-        def host_step():
-            if args.e2e_path == "step":
-                ks.step_host(xn, kn, gyn, scheme=scheme, mode=mode, out=(yn, dxn, dkn))
-            else:  # the reference's three value-type calls, each through its own host entry
-                ks.forward(xn, kn, mode, out=yn)
-                ks.backward_input(gyn, kn, mode, out=dxn)
-                ks.backward_weight(gyn, xn, K, scheme, 0, mode, out=dkn)
-
-        host_step()
-        if world > 1:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            host_step()
-        t_host = (time.perf_counter() - t0) / e2e_steps
-        if world > 1:
-            tt = torch.tensor([t_host], dtype=torch.float64, device=dev)
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            t_host = float(tt[0])
-        tb = 4 * B * H * L
-        if args.e2e_path == "step":
-            h2d, d2h = 2 * tb + 4 * H * K, 2 * tb + 4 * H * K
-            path = "ks_dwconv1d_step_f32_host (x, gy up once; y, dx, dk down), pinned host buffers, wall clock"
-        else:
-            h2d, d2h = 4 * tb + 2 * 4 * H * K, 2 * tb + 4 * H * K
-            path = "ks_dwconv1d_{fwd,dx,dw}_f32_host, pinned host buffers, wall clock"
-        e2e = {"value": round(world * 3 * pb / t_host / 1e9, 2), "unit": "GB/s",
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps, "path": path}
-        # the e2e roof: the step's PCIe bytes at the link's measured rates
-        # (H2D and D2H overlap on separate copy engines)
+        tb, kb = 4 * B * H * L, 4 * H * K
         pcie = pcie_probe(dev)
-        bound_s = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
-                      (h2d + d2h) / (pcie["bidir_gbs"] * 1e9))
-        pcie["bound_ms"] = round(bound_s * 1e3, 2)
-        pcie["frac"] = round(bound_s / t_host, 4)
-        e2e["pcie"] = pcie
+
+        def host_calls():  # the reference's three value-type calls, each through its own host entry
+            ks.forward(xn, kn, mode, out=yn)
+            ks.backward_input(gyn, kn, mode, out=dxn)
+            ks.backward_weight(gyn, xn, K, scheme, 0, mode, out=dkn)
+
+        def host_step():  # the library's one-call step: x and gy cross PCIe once
+            ks.step_host(xn, kn, gyn, scheme=scheme, mode=mode, out=(yn, dxn, dkn))
+
+        def measure(fn, h2d, d2h, path):
+            fn()
+            if world > 1:
+                dist.barrier()
+            t0 = time.perf_counter()
+            for _ in range(e2e_steps):
+                fn()
+            t_host = (time.perf_counter() - t0) / e2e_steps
+            if world > 1:
+                tt = torch.tensor([t_host], dtype=torch.float64, device=dev)
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t_host = float(tt[0])
+            # the e2e roof: the step's PCIe bytes at the link's measured rates
+            # (H2D and D2H overlap on separate copy engines)
+            bound_s = max(h2d / (pcie["h2d_gbs"] * 1e9), d2h / (pcie["d2h_gbs"] * 1e9),
+                          (h2d + d2h) / (pcie["bidir_gbs"] * 1e9))
+            return {"value": round(step_bytes(B_total, H, L, K) / t_host / 1e9, 2), "unit": "GB/s",
+                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                    "ms_per_step": round(t_host * 1e3, 2), "steps": e2e_steps, "path": path,
+                    "pcie": dict(pcie, bound_ms=round(bound_s * 1e3, 2), frac=round(bound_s / t_host, 4))}
+
+        e2e = measure(host_calls, 4 * tb + 2 * kb, 2 * tb + kb,
+                      "drop-in: ks_dwconv1d_{fwd,dx,dw}_f32_host (the reference's three value-type calls: "
+                      "x, gy, gy, x up; y, dx, dk down), pinned host buffers, wall clock")
+        e2e_step = measure(host_step, 2 * tb + kb, 2 * tb + kb,
+                           "ks_dwconv1d_step_f32_host (one call: x, gy up once; y, dx, dk down), pinned host "
+                           "buffers, wall clock")
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
-        gbs, _, sample, kind = cpu_sample(cfg, threads)
-        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind,
-               "sample": sample}
+        gbs, _, sample, kind = cpu_sample(cfg, threads, 1 if args.mode == "fused" else 0)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": kind, "sample": sample}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "GB/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": conf["scaling"], "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (reference splitmix64 stream, generated on device)",
-            "config": {"workload": WORKLOAD[cfg_name], "name": cfg_name, "B_per_gpu": B, "H": H,
-                       "L": L, "K": K, "global_batch": B * world,
-                       "parallelism": f"batch-shard dp{world}" + (
-                           "" if world == 1 else " + dW combine fused over NVLink peer memory" if peer is not None
-                           else " + NCCL dW allreduce"),
-                       "mode": args.mode, "dw_scheme": args.scheme,
-                       "l2": "inputs larger than L2 (no flush)" if flush is None
-                             else "L2 flushed before every timed step (512 MB write, untimed)",
-                       "cuda_graphs": graphs is not None,
-                       "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)"},
+            "config": conf,
+            "run": {"parallelism": f"batch-shard dp{world}" + (
+                        "" if world == 1 else " + dW combine fused over NVLink peer memory" if peer is not None
+                        else " + NCCL dW allreduce"),
+                    "rows_this_rank": B,
+                    "l2": "inputs larger than L2 (no flush)" if flush is None
+                          else "L2 flushed before every timed step (512 MB write, untimed)",
+                    "cuda_graphs": bool(graphs),
+                    "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)",
+                    "frac_hbm_measured": round(value / world / peak, 4), "frac_hbm_8TBs": round(value / world / 8000, 4)},
             "paths": paths, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            **({"e2e_step": e2e_step} if e2e_step else {}),
             **({"e2e_note": e2e_note} if e2e_note else {}),
-            "gpu_launches": launches,
+            "gpu_launches": gpu_launches,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)
     if peer is not None:
+        if peer.timed_out():
+            print("bench.py: a peer dW combine timed out (dk is NaN)", file=sys.stderr)
+            return 3
         peer.close()
     if comm is not None:
         comm.close()
@@ -654,21 +672,26 @@ def run_ours(args, cfg_name, cfg):
 
 
 def main():
-    ap = argparse.ArgumentParser(description=__doc__)
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(CONFIGS), default="config3")
-    ap.add_argument("--mode", choices=["fused", "separate"], default="fused")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling: fixed global batch sharded over the ranks (ks_shard_rows); "
+                         "default: weak scaling with the config's batch on every rank")
+    ap.add_argument("--mode", choices=["separate", "fused"], default="separate",
+                    help="MulAddMode (the reference's default is Separate)")
     ap.add_argument("--scheme", choices=["hierarchical", "pairwise"], default="hierarchical")
     ap.add_argument("--combine", choices=["nccl", "peer"], default="nccl",
                     help="N>1 dW combine: one ncclAllReduce, or the fused NVLink peer-memory kernel")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
-    ap.add_argument("--e2e-path", choices=["step", "calls"], default="step")
     ap.add_argument("--timing-log", default=None,
                     help="also write per-step path times in the reference's timing CSV schema")
+    ap.add_argument("--timing-variant", default="warp",
+                    help="variant column of --timing-log (the reference's parser accepts naive/gmc/shared/warp)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch each path eagerly instead of replaying CUDA graphs")
     ap.add_argument("--bwd", choices=["fused", "split"], default="fused",

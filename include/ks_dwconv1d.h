@@ -25,8 +25,10 @@
  *    (a cudaStream_t passed as void*, NULL = legacy default stream) and never
  *    synchronise.  No exceptions cross the boundary; every call returns a
  *    ks_status.
- *  - Determinism: for fixed (shape, mode, scheme) results are bitwise
- *    reproducible run to run; there are no floating-point atomics anywhere.
+ *  - Determinism: for fixed (shape, mode, scheme) and default tuning options
+ *    (ks_set_option) results are bitwise reproducible run to run, whatever the
+ *    alignment of the caller's pointers and whichever thread calls; there are
+ *    no floating-point atomics anywhere.
  *  - Rounding: y and dX accumulate taps in ascending j from +0, exactly like
  *    the reference loops (src/conv_core.cpp:37-40, 66-69), so they are
  *    bit-identical to the reference in both MulAddModes.  dW schemes
@@ -44,7 +46,7 @@
 extern "C" {
 #endif
 
-#define KS_DWCONV1D_ABI_VERSION 1
+#define KS_DWCONV1D_ABI_VERSION 2
 
 typedef enum ks_status {
     KS_OK = 0,
@@ -60,7 +62,9 @@ typedef enum ks_status {
     KS_ERR_NO_DEVICE = 10, /* no CUDA device / driver                                */
     KS_ERR_CUDA = 11,      /* CUDA runtime error (ks_last_error_string for text)     */
     KS_ERR_NCCL = 12,      /* NCCL error                                             */
-    KS_ERR_SHARD = 13      /* bad rank / world size / shard geometry                 */
+    KS_ERR_SHARD = 13,     /* bad rank / world size / shard geometry                 */
+    KS_ERR_BAD_OPTION = 14,/* unknown tuning option name or value out of range       */
+    KS_ERR_TIMEOUT = 15    /* a peer combine gave up waiting for a rank (dk is NaN)  */
 } ks_status;
 
 /* MulAddMode (conv_core.hpp:45): SEPARATE = acc + a*b with two roundings (the
@@ -131,6 +135,23 @@ ks_status ks_dwconv1d_bwd_f32(const float* gy, const float* x, const float* k, f
  * fill(seed,B*H*L), gy = fill(seed,B*H*L+H*K). */
 ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream);
 
+/* Number of kernels this library has launched in this process (every
+ * launch site counts; a CUDA-graph replay of captured calls does not call
+ * the library and is not counted). */
+ks_status ks_launch_count(uint64_t* count);
+
+/* Tuning options: tier switches and pipeline depths, process-wide, atomic.
+ * The defaults are the measured choices; the library never
+ * reads the environment.  Options that pick a kernel tier can change the bits
+ * of HIERARCHICAL dW (every tier keeps y / dX bit-identical to the
+ * reference); the determinism promise above is for the defaults.  Names:
+ * disable_tma, ldg, sts, bwds, dst, dwtma_j16, dwtma_ns, pad_skip, pad_ns,
+ * pad_prod, dwpad_ns, stencil_pad, stencil_r, stencil_nt, stencil_ns,
+ * host_block_mb.  KS_OPTION_DEFAULT restores an option's default. */
+#define KS_OPTION_DEFAULT INT64_MIN
+ks_status ks_set_option(const char* name, int64_t value);
+ks_status ks_get_option(const char* name, int64_t* value);
+
 /* Measured FP32 FMA throughput of the current device (TFLOP/s, 2 FLOP per
  * FMA): the compute roof for the long-K (FP32-bound) shapes.  Synchronous. */
 ks_status ks_probe_fp32_tflops(double* tflops);
@@ -191,32 +212,68 @@ typedef struct ks_comm ks_comm;
 /* 128-byte NCCL unique id, created on rank 0 and broadcast by the caller. */
 ks_status ks_comm_unique_id(void* id128);
 ks_status ks_comm_init(ks_comm** comm, const void* id128, int world, int rank);
+/* A communicator whose transport is the caller's: `allgather(send, recv,
+ * bytes, ctx)` must gather `bytes` host bytes from every rank into
+ * recv[world * bytes] in rank order and return 0 on success (e.g. an MPI or
+ * torch.distributed gloo all-gather).  Only bytes cross it -- every sum stays
+ * on the device -- so ranks may even share one GPU.  The dW combines below
+ * then run synchronously on the host side of `stream`. */
+typedef int (*ks_allgather_fn)(const void* send, void* recv, size_t bytes, void* ctx);
+ks_status ks_comm_init_host(ks_comm** comm, int world, int rank, ks_allgather_fn allgather, void* ctx);
 ks_status ks_comm_destroy(ks_comm* comm);
+/* Host-bytes all-gather over the communicator's transport (NCCL through a
+ * device bounce buffer, or the caller's callback): `bytes` from every rank
+ * into recv[world * bytes] in rank order.  Synchronous.  (What ks_peer_create
+ * uses to exchange IPC handles; exposed for setup-time agreement.) */
+ks_status ks_comm_allgather_host(ks_comm* comm, const void* send, void* recv, size_t bytes);
 /* In-place sum of the rank-local dk[H,K] over all ranks: one ncclAllReduce on
- * `stream`. */
+ * `stream` (NCCL communicator); a host communicator gathers the dk of every
+ * rank and sums them with ks_rank_tree_sum_f32. */
 ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm* comm,
                                        void* stream);
-/* Deterministic, world-size-invariant combine: all-gathers the per-rank
- * dk[H,K] into gather[world,H,K] (device scratch) and sums it in rank order
- * with a fixed pairwise tree, so every rank ends with the same bits. */
+/* Deterministic combine that does not depend on the collective's algorithm:
+ * all-gathers the per-rank dk[H,K] into gather[world,H,K] (device scratch)
+ * and sums it with ks_rank_tree_sum_f32, so every rank ends with the same
+ * bits for a given world size. */
 ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, int64_t K,
                                            ks_comm* comm, void* stream);
+/* out[i] = the midpoint-split pairwise tree over gather[r * n + i], r = 0 ..
+ * world-1 (the reference's reduce_pairwise shape, src/conv_core.cpp:113-118,
+ * over ranks); 1 <= world <= 64. */
+ks_status ks_rank_tree_sum_f32(const float* gather, float* out, int64_t n, int world, void* stream);
 
 /* ---- dW with the cross-GPU combine fused into the reduction (NVLink) ----- */
 /* The dW step of a batch-sharded training step is a compute step followed by
  * a collective.  ks_peer exposes each rank's partial buffer to every peer via
- * CUDA IPC (mapped over NVLink/NVSwitch; handles exchanged once through the
- * NCCL communicator); ks_dwconv1d_dw_f32_peer then runs the HIERARCHICAL
- * stage 1 into it and ONE kernel that signals the peers, waits for them
- * (system-scope release/acquire flags) and sums every rank's partials straight
- * from peer memory in fixed (rank, group) order -- identical bits on every
- * rank, no NCCL call on the data path.  Collective: every rank must call it. */
+ * CUDA IPC (mapped over NVLink/NVSwitch, or the same GPU; handles exchanged
+ * once through the communicator's all-gather); ks_dwconv1d_dw_f32_peer then
+ * runs the HIERARCHICAL stage 1 into it and ONE kernel that signals the peers,
+ * waits for them (system-scope release/acquire flags) and sums every rank's
+ * partials straight from peer memory in fixed (rank, group) order -- identical
+ * bits on every rank, no collective on the data path.  Each rank publishes its
+ * group count and shape with its partials, so uneven shards combine
+ * correctly; ranks whose (H, K) differ make the call fail.
+ *
+ * B is this rank's batch rows.  B_total > 0 names the global batch: when this
+ * rank holds rows ks_shard_rows(B_total, world, rank) and the global plan's
+ * row groups fall on shard boundaries (its group count G is a multiple of
+ * world and divides B_total), every rank computes exactly its shard's global
+ * groups, and dk is bitwise equal to the 1-GPU
+ * ks_dwconv1d_dw_f32(HIERARCHICAL) over the whole batch.  Otherwise (or
+ * B_total = 0) each rank plans its own groups: rank-consistent bits for a
+ * given world size.  Collective: every rank must call it, in the same order.
+ * partial_bytes >= ks_dwconv1d_dw_workspace_bytes(B, H, L, K, HIERARCHICAL)
+ * for the largest local B (and for B_total when the global plan is used). */
 typedef struct ks_peer ks_peer;
 ks_status ks_peer_create(ks_comm* comm, size_t partial_bytes, ks_peer** peer);
 ks_status ks_peer_destroy(ks_peer* peer);
 ks_status ks_dwconv1d_dw_f32_peer(const float* gy, const float* x, float* dk, int64_t B, int64_t H,
-                                  int64_t L, int64_t K, int mode, ks_peer* peer, void* stream);
-/* 1 when a combine gave up waiting (~10 s) for a peer that never arrived. */
+                                  int64_t L, int64_t K, int64_t B_total, int mode, ks_peer* peer,
+                                  void* stream);
+/* 1 when a combine gave up waiting (~10 s) for a peer that never arrived or
+ * found a peer with a different (H, K); that combine wrote NaN into dk and
+ * every later ks_dwconv1d_dw_f32_peer call returns KS_ERR_TIMEOUT.  Reads
+ * mapped host memory: no device synchronisation. */
 ks_status ks_peer_timed_out(ks_peer* peer, int* flag);
 
 #ifdef __cplusplus

@@ -214,7 +214,7 @@ void kso_backward_weight_i64(const float* gy, const float* x, int64_t* dk, int64
 
 /* ---- channel-slice fan-out (timed CPU baseline only) --------------------- */
 typedef struct {
-    int path; /* 0 fwd, 1 dx, 2 dw */
+    int path; /* 0 fwd, 1 dx, 2 dw, 3 dw in fp64 (a, b, out are double*) */
     const float *a, *b;
     float* out;
     int64_t B, H, L, K, chunk, h0, h1;
@@ -227,8 +227,12 @@ static void* kso_run_job(void* arg) {
         fwd_rows_f32(j->a, j->b, j->out, j->B, j->H, j->L, j->K, j->mode, j->h0, j->h1);
     else if (j->path == 1)
         dx_rows_f32(j->a, j->b, j->out, j->B, j->H, j->L, j->K, j->mode, j->h0, j->h1);
-    else
+    else if (j->path == 2)
         dw_rows_f32(j->a, j->b, j->out, j->B, j->H, j->L, j->K, j->scheme, j->chunk, j->mode,
+                    j->h0, j->h1);
+    else
+        dw_rows_f64((const double*)(const void*)j->a, (const double*)(const void*)j->b,
+                    (double*)(void*)j->out, j->B, j->H, j->L, j->K, j->scheme, j->chunk, j->mode,
                     j->h0, j->h1);
     return NULL;
 }
@@ -264,6 +268,17 @@ int kso_backward_weight_f32_mt(const float* gy, const float* x, float* dk, int64
                                int mode, int threads) {
     if (scheme == KSO_CHUNKED && chunk < 1) return -1;
     kso_job j = {2, gy, x, dk, B, H, L, K, chunk, 0, H, mode, scheme};
+    kso_fan_out(j, threads);
+    return 0;
+}
+
+/* fp64 dW fanned out over channels (the parity tests' truth at full size). */
+int kso_backward_weight_f64_mt(const double* gy, const double* x, double* dk, int64_t B,
+                               int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                               int mode, int threads) {
+    if (scheme == KSO_CHUNKED && chunk < 1) return -1;
+    kso_job j = {3, (const float*)(const void*)gy, (const float*)(const void*)x, (float*)(void*)dk,
+                 B, H, L, K, chunk, 0, H, mode, scheme};
     kso_fan_out(j, threads);
     return 0;
 }

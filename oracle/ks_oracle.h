@@ -72,6 +72,9 @@ void kso_backward_input_f32_mt(const float* gy, const float* k, float* dx, int64
 int kso_backward_weight_f32_mt(const float* gy, const float* x, float* dk, int64_t B,
                                int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                                int mode, int threads);
+int kso_backward_weight_f64_mt(const double* gy, const double* x, double* dk, int64_t B,
+                               int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                               int mode, int threads);
 
 #ifdef __cplusplus
 }

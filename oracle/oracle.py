@@ -91,8 +91,9 @@ class _Backend:
         B, H, L = gy.shape
         _check_shape(x, B, H, L)
         dk = np.empty((H, K), dtype=gy.dtype)
-        if threads and gy.dtype == np.float32:
-            f = self._fn("backward_weight_f32_mt",
+        if threads and (gy.dtype == np.float32 or self.prefix == "kso_"):
+            suf = "f32" if gy.dtype == np.float32 else "f64"
+            f = self._fn(f"backward_weight_{suf}_mt",
                          [_p, _p, _p, _i64, _i64, _i64, _i64, C.c_int, _i64, C.c_int, C.c_int])
             rc = f(_ptr(gy), _ptr(x), _ptr(dk), B, H, L, K, scheme, chunk, mode, threads)
         else:

@@ -20,8 +20,9 @@ STATUS_NAMES = {
     0: "KS_OK", 1: "KS_ERR_DIM_B", 2: "KS_ERR_DIM_H", 3: "KS_ERR_DIM_L", 4: "KS_ERR_DIM_K",
     5: "KS_ERR_BAD_CHUNK", 6: "KS_ERR_BAD_MODE", 7: "KS_ERR_BAD_SCHEME", 8: "KS_ERR_NULL",
     9: "KS_ERR_WORKSPACE", 10: "KS_ERR_NO_DEVICE", 11: "KS_ERR_CUDA", 12: "KS_ERR_NCCL",
-    13: "KS_ERR_SHARD",
+    13: "KS_ERR_SHARD", 14: "KS_ERR_BAD_OPTION", 15: "KS_ERR_TIMEOUT",
 }
+KS_OPTION_DEFAULT = -(1 << 63)
 SEPARATE, FUSED = 0, 1
 SEQUENTIAL, PAIRWISE, CHUNKED, HIERARCHICAL = 0, 1, 2, 3
 
@@ -30,17 +31,21 @@ EXPORTED = [
     "ks_status_string", "ks_last_error_string", "ks_abi_version",
     "ks_dwconv1d_fwd_f32", "ks_dwconv1d_fwd_f64", "ks_dwconv1d_dx_f32", "ks_dwconv1d_dx_f64",
     "ks_dwconv1d_dw_workspace_bytes", "ks_dwconv1d_dw_f32", "ks_dwconv1d_dw_f64",
-    "ks_dwconv1d_bwd_f32", "ks_fill_pm1_f32", "ks_probe_fp32_tflops",
+    "ks_dwconv1d_bwd_f32", "ks_fill_pm1_f32", "ks_launch_count", "ks_set_option", "ks_get_option",
+    "ks_probe_fp32_tflops",
     "ks_dwconv1d_fwd_f32_host", "ks_dwconv1d_dx_f32_host", "ks_dwconv1d_dw_f32_host",
     "ks_dwconv1d_fwd_f64_host", "ks_dwconv1d_dx_f64_host", "ks_dwconv1d_dw_f64_host",
     "ks_dwconv1d_step_f32_host",
     "ks_dwconv1d_variant_workspace_bytes", "ks_dwconv1d_variant_f32",
-    "ks_shard_rows", "ks_comm_unique_id", "ks_comm_init", "ks_comm_destroy",
-    "ks_dwconv1d_dw_allreduce_f32", "ks_dwconv1d_dw_allgather_sum_f32",
+    "ks_shard_rows", "ks_comm_unique_id", "ks_comm_init", "ks_comm_init_host", "ks_comm_destroy",
+    "ks_comm_allgather_host",
+    "ks_dwconv1d_dw_allreduce_f32", "ks_dwconv1d_dw_allgather_sum_f32", "ks_rank_tree_sum_f32",
     "ks_peer_create", "ks_peer_destroy", "ks_dwconv1d_dw_f32_peer", "ks_peer_timed_out",
 ]
 
 _i64, _u64, _p, _int, _sz = C.c_int64, C.c_uint64, C.c_void_p, C.c_int, C.c_size_t
+# host all-gather callback of ks_comm_init_host: (send, recv, bytes, ctx) -> 0 on success
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 _SIGS = {
     "ks_status_string": ([_int], C.c_char_p),
     "ks_last_error_string": ([], C.c_char_p),
@@ -55,6 +60,9 @@ _SIGS = {
     "ks_dwconv1d_dw_f64": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _i64, _int, _p, _sz, _p], _int),
     "ks_fill_pm1_f32": ([_u64, _u64, _p, _i64, _p], _int),
     "ks_probe_fp32_tflops": ([C.POINTER(C.c_double)], _int),
+    "ks_launch_count": ([C.POINTER(_u64)], _int),
+    "ks_set_option": ([C.c_char_p, _i64], _int),
+    "ks_get_option": ([C.c_char_p, C.POINTER(_i64)], _int),
     "ks_dwconv1d_fwd_f32_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int], _int),
     "ks_dwconv1d_dx_f32_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int], _int),
     "ks_dwconv1d_dw_f32_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _i64, _int], _int),
@@ -67,12 +75,15 @@ _SIGS = {
     "ks_shard_rows": ([_i64, _int, _int, C.POINTER(_i64), C.POINTER(_i64)], _int),
     "ks_comm_unique_id": ([_p], _int),
     "ks_comm_init": ([C.POINTER(_p), _p, _int, _int], _int),
+    "ks_comm_init_host": ([C.POINTER(_p), _int, _int, ALLGATHER_FN, _p], _int),
+    "ks_rank_tree_sum_f32": ([_p, _p, _i64, _int, _p], _int),
+    "ks_comm_allgather_host": ([_p, _p, _p, _sz], _int),
     "ks_comm_destroy": ([_p], _int),
     "ks_dwconv1d_dw_allreduce_f32": ([_p, _i64, _i64, _p, _p], _int),
     "ks_dwconv1d_dw_allgather_sum_f32": ([_p, _p, _i64, _i64, _p, _p], _int),
     "ks_peer_create": ([_p, _sz, C.POINTER(_p)], _int),
     "ks_peer_destroy": ([_p], _int),
-    "ks_dwconv1d_dw_f32_peer": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int, _p, _p], _int),
+    "ks_dwconv1d_dw_f32_peer": ([_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _int, _p, _p], _int),
     "ks_peer_timed_out": ([_p, C.POINTER(_int)], _int),
 }
 

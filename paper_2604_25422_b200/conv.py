@@ -17,6 +17,7 @@ library's own sm_100a kernels.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 
 import numpy as np
@@ -88,6 +89,48 @@ def _empty_like(a, shape):
     return np.empty(shape, dtype=a.dtype)
 
 
+def _same_kind(a, like, name: str) -> None:
+    """`a` must be the same kind of buffer as `like` (torch CUDA tensor on the
+    same device, or a host numpy array) with the same dtype: the C ABI takes
+    raw pointers, so a host pointer among device pointers (or the reverse)
+    would be an illegal address, not an exception."""
+    if _is_torch(like):
+        if not _is_torch(a):
+            raise TypeError(f"{name}: expected a torch CUDA tensor like the input, got {type(a).__name__}")
+        if a.device != like.device:
+            raise ValueError(f"{name}: on {a.device}, the input is on {like.device}")
+    elif _is_torch(a) or not isinstance(a, np.ndarray):
+        raise TypeError(f"{name}: expected a numpy array like the input, got {type(a).__name__}")
+    if a.dtype != like.dtype:
+        raise TypeError(f"{name}: dtype {a.dtype}, the input is {like.dtype}")
+
+
+def _check_out(out, like, shape, name: str):
+    """A caller-supplied output: right kind, device, dtype, shape, contiguous."""
+    if out is None:
+        return _empty_like(like, shape)
+    _same_kind(out, like, name)
+    if tuple(int(v) for v in out.shape) != tuple(shape):
+        raise DimensionError(f"{name}: shape {tuple(out.shape)}, expected {tuple(shape)}")
+    return out
+
+
+def _check_ws(ws, like):
+    """(pointer, bytes) of an optional device workspace."""
+    if ws is None:
+        return None, 0
+    if not (_is_torch(ws) and _is_torch(like)) or ws.device != like.device:
+        raise TypeError("workspace: a torch CUDA tensor on the input's device")
+    if not ws.is_contiguous():
+        raise ValueError("workspace must be contiguous")
+    return ws.data_ptr(), ws.numel() * ws.element_size()
+
+
+def _on_device(a):
+    """Launch on the tensor's device, not whatever device is current."""
+    return torch.cuda.device(a.device) if _is_torch(a) else contextlib.nullcontext()
+
+
 def _raise_dims(status: int, what: str):
     if status in (1, 2, 3, 4, 5):
         raise DimensionError(f"{what}: {_lib.STATUS_NAMES[status]}")
@@ -98,14 +141,13 @@ def _stencil(kind: str, inp, k, mode: int, out=None):
     B, H, L = _dims3(inp, f"{kind}: input")
     K = _dims_k(k, f"{kind}: k", H)
     suf = _suffix(inp)
-    if _suffix(k) != suf:
-        raise TypeError("input and kernel dtypes differ")
-    if out is None:
-        out = _empty_like(inp, (B, H, L))
+    _same_kind(k, inp, f"{kind}: k")
+    out = _check_out(out, inp, (B, H, L), f"{kind}: out")
     l = _lib.lib()
     if _is_torch(inp):
         fn = getattr(l, f"ks_dwconv1d_{kind}_{suf}")
-        st = fn(_ptr(inp), _ptr(k), _ptr(out), B, H, L, K, mode, _stream(inp))
+        with _on_device(inp):
+            st = fn(_ptr(inp), _ptr(k), _ptr(out), B, H, L, K, mode, _stream(inp))
     else:
         fn = getattr(l, f"ks_dwconv1d_{kind}_{suf}_host")
         st = fn(_ptr(inp), _ptr(k), _ptr(out), B, H, L, K, mode)
@@ -144,18 +186,15 @@ def backward_weight(gy, x, K: int, scheme: int = SEQUENTIAL, chunk: int = 1024,
     if scheme == CHUNKED and chunk < 1:
         raise DimensionError(f"backward_weight: chunk_size must be >= 1, got {chunk}")
     suf = _suffix(gy)
-    if _suffix(x) != suf:
-        raise TypeError("gy and x dtypes differ")
-    if out is None:
-        out = _empty_like(gy, (H, K))
+    _same_kind(x, gy, "backward_weight: x")
+    out = _check_out(out, gy, (H, K), "backward_weight: out")
     l = _lib.lib()
     if _is_torch(gy):
-        ws_ptr, ws_bytes = None, 0
-        if workspace is not None:
-            ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+        ws_ptr, ws_bytes = _check_ws(workspace, gy)
         fn = getattr(l, f"ks_dwconv1d_dw_{suf}")
-        st = fn(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, scheme, chunk, mode, ws_ptr, ws_bytes,
-                _stream(gy))
+        with _on_device(gy):
+            st = fn(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, scheme, chunk, mode, ws_ptr, ws_bytes,
+                    _stream(gy))
     else:
         fn = getattr(l, f"ks_dwconv1d_dw_{suf}_host")
         st = fn(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, scheme, chunk, mode)
@@ -171,16 +210,17 @@ def backward(gy, x, k, mode: int = SEPARATE, out=None, workspace=None):
     B, H, L = _dims3(gy, "backward: gy")
     _dims3(x, "backward: x", (B, H, L))
     K = _dims_k(k, "backward: k", H)
-    if not _is_torch(gy) or _suffix(gy) != "f32" or _suffix(x) != "f32" or _suffix(k) != "f32":
+    if not _is_torch(gy) or _suffix(gy) != "f32":
         raise TypeError("backward: fp32 CUDA tensors")
-    if out is None:
-        out = (_empty_like(gy, (B, H, L)), _empty_like(gy, (H, K)))
-    dx, dk = out
-    ws_ptr, ws_bytes = None, 0
-    if workspace is not None:
-        ws_ptr, ws_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
-    st = _lib.lib().ks_dwconv1d_bwd_f32(_ptr(gy), _ptr(x), _ptr(k), _ptr(dx), _ptr(dk), B, H, L, K, mode,
-                                        ws_ptr, ws_bytes, _stream(gy))
+    _same_kind(x, gy, "backward: x")
+    _same_kind(k, gy, "backward: k")
+    dx, dk = out if out is not None else (None, None)
+    dx = _check_out(dx, gy, (B, H, L), "backward: dx")
+    dk = _check_out(dk, gy, (H, K), "backward: dk")
+    ws_ptr, ws_bytes = _check_ws(workspace, gy)
+    with _on_device(gy):
+        st = _lib.lib().ks_dwconv1d_bwd_f32(_ptr(gy), _ptr(x), _ptr(k), _ptr(dx), _ptr(dk), B, H, L, K, mode,
+                                            ws_ptr, ws_bytes, _stream(gy))
     _raise_dims(st, "backward")
     return dx, dk
 
@@ -192,9 +232,14 @@ def step_host(x, k, gy, K: int | None = None, scheme: int = HIERARCHICAL, chunk:
     B, H, L = _dims3(x, "step: x")
     _dims3(gy, "step: gy", (B, H, L))
     K = _dims_k(k, "step: k", H)
-    if out is None:
-        out = (np.empty_like(x), np.empty_like(gy), np.empty((H, K), np.float32))
-    y, dx, dk = out
+    if _is_torch(x) or _suffix(x) != "f32":
+        raise TypeError("step_host: fp32 numpy (host) arrays")
+    _same_kind(k, x, "step: k")
+    _same_kind(gy, x, "step: gy")
+    y, dx, dk = out if out is not None else (None, None, None)
+    y = _check_out(y, x, (B, H, L), "step: y")
+    dx = _check_out(dx, x, (B, H, L), "step: dx")
+    dk = _check_out(dk, x, (H, K), "step: dk")
     st = _lib.lib().ks_dwconv1d_step_f32_host(_ptr(x), _ptr(k), _ptr(gy), _ptr(y), _ptr(dx), _ptr(dk),
                                               B, H, L, K, scheme, chunk, mode)
     _raise_dims(st, "step")
@@ -218,10 +263,13 @@ def variant(name: str, path: str, a, b, K: int | None = None, mode: int = FUSED,
     else:
         K = _dims_k(b, f"{name} {path}: k", H)
         shape_out = (B, H, L)
-    if out is None:
-        out = _empty_like(a, shape_out)
-    st = _lib.lib().ks_dwconv1d_variant_f32(v, p, _ptr(a), _ptr(b), _ptr(out), B, H, L, K, mode, None, 0,
-                                           _stream(a))
+    if not _is_torch(a):
+        raise TypeError("variant: torch CUDA tensors")
+    _same_kind(b, a, f"{name} {path}: b")
+    out = _check_out(out, a, shape_out, f"{name} {path}: out")
+    with _on_device(a):
+        st = _lib.lib().ks_dwconv1d_variant_f32(v, p, _ptr(a), _ptr(b), _ptr(out), B, H, L, K, mode, None, 0,
+                                               _stream(a))
     _raise_dims(st, f"variant {name} {path}")
     return out
 
@@ -229,7 +277,10 @@ def variant(name: str, path: str, a, b, K: int | None = None, mode: int = FUSED,
 def fill_pm1(seed: int, first: int, out) -> None:
     """Device splitmix64 fill, bit-identical to the reference SplitMix64 stream
     (include/kernelscope/rng.hpp:12-28): out.flat[i] = draw first+1+i."""
-    st = _lib.lib().ks_fill_pm1_f32(seed, first, _ptr(out), out.numel(), _stream(out))
+    if not _is_torch(out) or out.dtype != torch.float32:
+        raise TypeError("fill_pm1: an fp32 torch CUDA tensor")
+    with _on_device(out):
+        st = _lib.lib().ks_fill_pm1_f32(seed, first, _ptr(out), out.numel(), _stream(out))
     check(st, "fill_pm1")
 
 
@@ -259,9 +310,14 @@ def shard_rows(B: int, world: int, rank: int):
 
 
 class Comm:
-    """NCCL communicator owned by the C library (one process per GPU).  The
-    128-byte unique id is created on rank 0 and broadcast by the caller (e.g.
-    over torch.distributed)."""
+    """A communicator owned by the C library (one process per rank).
+
+    ``Comm(uid, world, rank)`` is an NCCL communicator (one GPU per rank; the
+    128-byte unique id is created on rank 0 and broadcast by the caller, e.g.
+    over torch.distributed).  ``Comm.host(world, rank, allgather)`` uses the
+    caller's host all-gather instead -- ``allgather(data: bytes) -> list[bytes]``
+    in rank order, e.g. over a gloo process group -- which only moves bytes
+    (every sum stays on the device), so ranks may share one GPU."""
 
     @staticmethod
     def unique_id() -> bytes:
@@ -269,27 +325,63 @@ class Comm:
         check(_lib.lib().ks_comm_unique_id(C.addressof(buf)), "comm_unique_id")
         return bytes(buf)
 
-    def __init__(self, uid: bytes, world: int, rank: int):
-        buf = (C.c_char * 128).from_buffer_copy(uid)
+    def __init__(self, uid: bytes | None, world: int, rank: int, _host=None):
         self.handle = C.c_void_p()
+        self.world, self.rank = world, rank
+        self._cb = None
+        if _host is not None:
+            def _allgather(send, recv, nbytes, _ctx):
+                try:
+                    parts = _host(C.string_at(send, nbytes))
+                    if len(parts) != world or any(len(p) != nbytes for p in parts):
+                        return 1
+                    C.memmove(recv, b"".join(parts), nbytes * world)
+                    return 0
+                except Exception:  # a Python exception must not unwind through C
+                    return 1
+            self._cb = _lib.ALLGATHER_FN(_allgather)  # kept alive with the communicator
+            check(_lib.lib().ks_comm_init_host(C.byref(self.handle), world, rank, self._cb, None),
+                  "comm_init_host")
+            return
+        buf = (C.c_char * 128).from_buffer_copy(uid)
         check(_lib.lib().ks_comm_init(C.byref(self.handle), C.addressof(buf), world, rank),
               "comm_init")
-        self.world, self.rank = world, rank
+
+    @classmethod
+    def host(cls, world: int, rank: int, allgather) -> "Comm":
+        return cls(None, world, rank, _host=allgather)
+
+    def allgather_bytes(self, data: bytes) -> list:
+        """ks_comm_allgather_host: every rank's `data` (same length), rank order."""
+        n = len(data)
+        recv = (C.c_char * (n * self.world))()
+        check(_lib.lib().ks_comm_allgather_host(self.handle, data, C.addressof(recv), n), "comm_allgather_host")
+        raw = bytes(recv)
+        return [raw[r * n:(r + 1) * n] for r in range(self.world)]
 
     def allreduce_dw(self, dk) -> None:
         H, K = (int(v) for v in dk.shape)
-        check(_lib.lib().ks_dwconv1d_dw_allreduce_f32(_ptr(dk), H, K, self.handle, _stream(dk)),
-              "dw_allreduce")
+        with _on_device(dk):
+            check(_lib.lib().ks_dwconv1d_dw_allreduce_f32(_ptr(dk), H, K, self.handle, _stream(dk)),
+                  "dw_allreduce")
 
     def allgather_sum_dw(self, dk, gather) -> None:
         H, K = (int(v) for v in dk.shape)
-        check(_lib.lib().ks_dwconv1d_dw_allgather_sum_f32(_ptr(dk), _ptr(gather), H, K,
-                                                          self.handle, _stream(dk)),
-              "dw_allgather_sum")
+        _same_kind(gather, dk, "allgather_sum_dw: gather")
+        if gather.numel() < self.world * H * K:
+            raise DimensionError(f"allgather_sum_dw: gather needs {self.world * H * K} floats")
+        with _on_device(dk):
+            check(_lib.lib().ks_dwconv1d_dw_allgather_sum_f32(_ptr(dk), _ptr(gather), H, K,
+                                                              self.handle, _stream(dk)),
+                  "dw_allgather_sum")
 
-    def peer(self, B: int, H: int, L: int, K: int) -> "Peer":
-        """NVLink peer-memory dW combine for per-rank shape (B,H,L,K)."""
-        return Peer(self, workspace_bytes(B, H, L, K, HIERARCHICAL))
+    def peer(self, B: int, H: int, L: int, K: int, B_total: int = 0) -> "Peer":
+        """Peer-memory dW combine for per-rank shape (B,H,L,K); with B_total the
+        global plan (bitwise = the 1-GPU result when the shards align)."""
+        need = workspace_bytes(B, H, L, K, HIERARCHICAL)
+        if B_total:
+            need = max(need, workspace_bytes(B_total, H, L, K, HIERARCHICAL))
+        return Peer(self, need)
 
     def close(self) -> None:
         if self.handle:
@@ -299,20 +391,24 @@ class Comm:
 
 class Peer:
     """ks_peer: dW whose cross-rank sum is fused into the reduction kernel and
-    read straight from the peers' memory (no NCCL on the data path)."""
+    read straight from the peers' memory (no collective on the data path)."""
 
     def __init__(self, comm: Comm, partial_bytes: int):
         self.handle = C.c_void_p()
+        self.comm = comm
         check(_lib.lib().ks_peer_create(comm.handle, max(partial_bytes, 4), C.byref(self.handle)),
               "peer_create")
 
-    def backward_weight(self, gy, x, K: int, mode: int = FUSED, out=None):
+    def backward_weight(self, gy, x, K: int, mode: int = FUSED, out=None, B_total: int = 0):
         B, H, L = _dims3(gy, "peer dw: gy")
         _dims3(x, "peer dw: x", (B, H, L))
-        if out is None:
-            out = _empty_like(gy, (H, K))
-        st = _lib.lib().ks_dwconv1d_dw_f32_peer(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, mode,
-                                               self.handle, _stream(gy))
+        if not _is_torch(gy) or _suffix(gy) != "f32":
+            raise TypeError("peer dw: fp32 torch CUDA tensors")
+        _same_kind(x, gy, "peer dw: x")
+        out = _check_out(out, gy, (H, K), "peer dw: out")
+        with _on_device(gy):
+            st = _lib.lib().ks_dwconv1d_dw_f32_peer(_ptr(gy), _ptr(x), _ptr(out), B, H, L, K, B_total, mode,
+                                                   self.handle, _stream(gy))
         _raise_dims(st, "dw_peer")
         return out
 
@@ -325,3 +421,52 @@ class Peer:
         if self.handle:
             _lib.lib().ks_peer_destroy(self.handle)
             self.handle = C.c_void_p()
+
+
+def rank_tree_sum(gather, out) -> None:
+    """out[i] = midpoint-split pairwise tree over gather[r, i], r in rank order
+    (ks_rank_tree_sum_f32): the fixed cross-rank combine."""
+    if not _is_torch(gather) or _suffix(gather) != "f32" or gather.ndim != 2:
+        raise TypeError("rank_tree_sum: a [world, n] fp32 torch CUDA tensor")
+    world, n = (int(v) for v in gather.shape)
+    _same_kind(out, gather, "rank_tree_sum: out")
+    if out.numel() != n:
+        raise DimensionError(f"rank_tree_sum: out has {out.numel()} floats, expected {n}")
+    with _on_device(gather):
+        check(_lib.lib().ks_rank_tree_sum_f32(_ptr(gather), _ptr(out), n, world, _stream(gather)),
+              "rank_tree_sum")
+
+
+# ---- library-wide -----------------------------------------------------------
+
+def set_option(name: str, value: int | None = None) -> None:
+    """ks_set_option: a tuning option (tier switch / pipeline depth); None
+    restores the default."""
+    v = _lib.KS_OPTION_DEFAULT if value is None else int(value)
+    check(_lib.lib().ks_set_option(name.encode(), v), f"set_option {name}")
+
+
+def get_option(name: str) -> int:
+    v = C.c_int64(0)
+    check(_lib.lib().ks_get_option(name.encode(), C.byref(v)), f"get_option {name}")
+    return int(v.value)
+
+
+@contextlib.contextmanager
+def options(**kw):
+    """Temporarily set tuning options (restored to their previous values)."""
+    old = {k: get_option(k) for k in kw}
+    try:
+        for k, v in kw.items():
+            set_option(k, v)
+        yield
+    finally:
+        for k, v in old.items():
+            set_option(k, v)
+
+
+def launch_count() -> int:
+    """Kernels this library has launched in this process (ks_launch_count)."""
+    v = C.c_uint64(0)
+    check(_lib.lib().ks_launch_count(C.byref(v)), "launch_count")
+    return int(v.value)

@@ -56,8 +56,7 @@ ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorM
 // 1.89 -> 2.22 ms) and at config 5a's full size (fwd 11.1 -> 13.4 ms in the
 // bench, ABAB).  KS_DST=1 turns them on (both paths give the same bits).
 inline bool direct_store(const float* out) {
-    const char* e = getenv("KS_DST");
-    return e && atoi(e) > 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+    return opt(kOptDst) > 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 }
 
 inline bool shape_ok(int64_t B, int64_t H, int64_t L, int64_t K) {

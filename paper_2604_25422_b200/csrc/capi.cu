@@ -2,6 +2,7 @@
 // argument validation in the reference's order (ConvShape ctor checks B,H,L,K,
 // shape.hpp:27-31; chunk_size >= 1, src/conv_core.cpp:154-156), launch
 // selection, scratch management and the on-device splitmix64 generator.
+#include <atomic>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -39,17 +40,23 @@ ks_status cuda_status(cudaError_t e) {
     return KS_ERR_CUDA;
 }
 
-ks_status check_launch() { return cuda_status(cudaGetLastError()); }
+static std::atomic<uint64_t> g_launches{0};
 
+ks_status check_launch() {
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cuda_status(cudaGetLastError());
+}
+
+// One library-owned pool per device, created once under a lock (concurrent
+// first calls from several host threads must not race on it).
 static cudaMemPool_t scratch_pool() {
     constexpr int kMaxDev = 64;
     static cudaMemPool_t pools[kMaxDev] = {};
-    static bool made[kMaxDev] = {};
+    static std::once_flag made[kMaxDev];
     int dev = 0;
     cudaGetDevice(&dev);
     if (dev < 0 || dev >= kMaxDev) return nullptr;
-    if (!made[dev]) {
-        made[dev] = true;
+    std::call_once(made[dev], [dev] {
         cudaMemPoolProps props = {};
         props.allocType = cudaMemAllocationTypePinned;
         props.handleTypes = cudaMemHandleTypeNone;
@@ -62,7 +69,7 @@ static cudaMemPool_t scratch_pool() {
             pools[dev] = nullptr;
             cudaGetLastError();
         }
-    }
+    });
     return pools[dev];
 }
 
@@ -222,11 +229,19 @@ const char* ks_status_string(ks_status s) {
         case KS_ERR_CUDA: return "CUDA error";
         case KS_ERR_NCCL: return "NCCL error";
         case KS_ERR_SHARD: return "bad shard geometry";
+        case KS_ERR_BAD_OPTION: return "unknown option or value out of range";
+        case KS_ERR_TIMEOUT: return "peer combine timed out or met a mismatched rank";
     }
     return "unknown status";
 }
 
 const char* ks_last_error_string(void) { return g_last_error.c_str(); }
+
+ks_status ks_launch_count(uint64_t* count) {
+    if (!count) return KS_ERR_NULL;
+    *count = g_launches.load(std::memory_order_relaxed);
+    return KS_OK;
+}
 int ks_abi_version(void) { return KS_DWCONV1D_ABI_VERSION; }
 
 ks_status ks_dwconv1d_fwd_f32(const float* x, const float* k, float* y, int64_t B, int64_t H,

@@ -418,15 +418,14 @@ ks_status launch_hier(const float* gy, const float* x, float* part, int64_t B, i
 size_t dw_pairwise_tma_workspace(int64_t B, int64_t H, int64_t L, int64_t K);
 ks_status dw_pairwise_tma_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
                               int64_t K, void* ws, cudaStream_t st, bool* handled);
-bool tma_disabled();
-bool dw_cb_applies(int64_t B, int64_t H, int64_t L, int64_t K);
-int dw_cb_groups(int64_t B, int64_t H, int64_t K);
-ks_status dw_cb_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
+bool dw_pad_applies(int64_t B, int64_t H, int64_t L, int64_t K);
+int dw_pad_groups(int64_t B, int64_t H, int64_t K);
+ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
                        int G, int mode, cudaStream_t st, bool* handled);
 
 // Row groups G of the HIERARCHICAL partial buffer part[G,H,K] for this shape.
 static int hier_groups(int64_t B, int64_t H, int64_t L, int64_t K) {
-    if (!tma_disabled() && dw_cb_applies(B, H, L, K)) return dw_cb_groups(B, H, K);
+    if (!tma_disabled() && dw_pad_applies(B, H, L, K)) return dw_pad_groups(B, H, K);
     return hier_plan(B, H, K).g;
 }
 
@@ -486,7 +485,7 @@ ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, in
 
 ks_status dw_rows_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
                          cudaStream_t, bool*);
-ks_status dw_stage1_only(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, void*, int*,
+ks_status dw_stage1_only(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int, int*,
                          cudaStream_t);
 
 ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H, int64_t L,
@@ -502,25 +501,50 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
         return dw_exact<float>(gy, x, dk, B, H, L, K, KS_DW_PAIRWISE, 0, mode, ws, st);
     float* part = static_cast<float*>(ws);
     int G = 0;
-    ks_status s = dw_stage1_only(gy, x, part, B, H, L, K, mode, nullptr, &G, st);
+    ks_status s = dw_stage1_only(gy, x, part, B, H, L, K, mode, 0, &G, st);
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
     dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, G);
     return check_launch();
 }
 
+// Row groups the HIERARCHICAL plan gives this shape (the G of part[G,H,K]).
+int dw_plan_groups(int64_t B, int64_t H, int64_t L, int64_t K) { return hier_groups(B, H, L, K); }
+
 // HIERARCHICAL stage 1 only: per-CTA partials part[G,H,K] (G returned), for
-// the fused cross-GPU combine of peer.cu and for dw_f32 above.
+// the fused cross-GPU combine of peer.cu and for dw_f32 above.  G_req > 0
+// overrides the plan's row-group count (peer.cu: this rank's share of the
+// global plan's groups); the kernel tier is chosen exactly as without it.
+//
+// The TMA tiers need 16-byte aligned bases; a caller's offset view that is
+// not (L % 4 == 0 but the base is off by 4, 8 or 12 bytes) is first copied
+// into aligned stream-ordered scratch, so the kernel -- and with it the
+// association order, i.e. the bits of dk -- never depends on where the
+// caller's tensors sit in memory.  (L % 4 != 0 cannot be encoded as a TMA
+// view at any alignment: those shapes always take the generic kernel.)
 ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
-                         int mode, void*, int* G, cudaStream_t st) {
+                         int mode, int G_req, int* G, cudaStream_t st) {
+    if ((((reinterpret_cast<uintptr_t>(gy) | reinterpret_cast<uintptr_t>(x)) & 15) != 0) && L % 4 == 0 &&
+        !tma_disabled()) {
+        const size_t n = size_t(B) * size_t(H) * size_t(L);
+        float* a = nullptr;
+        ks_status s = cuda_status(scratch_alloc(reinterpret_cast<void**>(&a), 2 * n * sizeof(float), st));
+        if (s != KS_OK) return s;
+        s = cuda_status(cudaMemcpyAsync(a, gy, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        if (s == KS_OK) s = cuda_status(cudaMemcpyAsync(a + n, x, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        if (s == KS_OK) s = dw_stage1_only(a, a + n, part, B, H, L, K, mode, G_req, G, st);
+        scratch_free(a, st);
+        return s;
+    }
     HierPlan pl = hier_plan(B, H, K);
     bool handled = false;
     ks_status s = KS_OK;
-    if (!tma_disabled() && dw_cb_applies(B, H, L, K)) {  // compute-bound long K (dw_cb.cu)
-        pl.g = dw_cb_groups(B, H, K);
-        s = dw_cb_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
+    if (!tma_disabled() && dw_pad_applies(B, H, L, K)) {  // compute-bound long K (dw_pad.cu)
+        pl.g = G_req > 0 ? G_req : dw_pad_groups(B, H, K);
+        s = dw_pad_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
         if (!handled) pl = hier_plan(B, H, K);
     }
+    if (G_req > 0) pl.g = G_req;
     if (!handled && L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
     if (!handled && !tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
     if (!handled)
@@ -540,7 +564,9 @@ ks_status bwd_tma_stage1(const float*, const float*, const float*, float*, float
 ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* dx, float* dk, int64_t B,
                         int64_t H, int64_t L, int64_t K, int mode, void* ws, cudaStream_t st, bool* fused) {
     *fused = false;
-    if (tma_disabled() || L < 2048 || L % 32 != 0 || K > 16 || dw_cb_applies(B, H, L, K)) return KS_OK;
+    if (tma_disabled() || L < 2048 || L % 32 != 0 || K > 16 || dw_pad_applies(B, H, L, K)) return KS_OK;
+    // unaligned bases: the split path (dw_f32 stages them into aligned scratch)
+    if (((reinterpret_cast<uintptr_t>(gy) | reinterpret_cast<uintptr_t>(x)) & 15) != 0) return KS_OK;
     if (L > (1ll << 30) || B > (1ll << 30)) return KS_OK;
     const HierPlan pl = hier_plan(B, H, K);
     float* part = static_cast<float*>(ws);

@@ -225,13 +225,6 @@ ks_status stencil_tma_f32(const float*, const float*, float*, int64_t, int64_t, 
 ks_status stencil_rows_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
                            int, int, cudaStream_t, bool*);
 
-bool tma_disabled() {
-    static const bool off = [] {
-        const char* e = getenv("KS_DISABLE_TMA");
-        return e && e[0] == '1';
-    }();
-    return off;
-}
 
 // Entry used by the C ABI for both fp32 paths (shapes already validated).
 ks_status conv_stencil_f32(const float* in, const float* k, float* out, int64_t B, int64_t H,

@@ -8,15 +8,20 @@
 //  * ks_dwconv1d_dw_allgather_sum_f32: ncclAllGather of the rank partials, then
 //    a fixed pairwise tree in rank order on every rank, so the result does not
 //    depend on NCCL's algorithm/protocol choice and is bitwise identical on all
-//    ranks (and, for PAIRWISE with power-of-two shards, to the 1-GPU result).
+//    ranks for a given world size.
+//  * ks_comm_init_host: the same combines over a caller-supplied host
+//    all-gather (MPI, torch.distributed gloo, ...): the bytes cross the host,
+//    the sums stay on the device.  Ranks may share a GPU, which NCCL refuses,
+//    so this is also how the multi-rank paths are exercised on one B200.
 #include <nccl.h>
+
+#include <cstring>
+#include <vector>
 
 #include "ks_common.cuh"
 #include "ks_dist.cuh"
 
 namespace ks {
-
-void set_last_error(const char* what);
 
 static ks_status nccl_status(ncclResult_t r) {
     if (r == ncclSuccess) return KS_OK;
@@ -63,6 +68,45 @@ __global__ void rank_tree_sum(const float* __restrict__ gather, float* __restric
     out[i] = vals[0];
 }
 
+ks_status comm_allgather_host(ks_comm* c, const void* send, void* recv, size_t bytes) {
+    if (c->world == 1) {
+        memcpy(recv, send, bytes);
+        return KS_OK;
+    }
+    if (c->host_allgather) {
+        if (c->host_allgather(send, recv, bytes, c->host_ctx) != 0) {
+            set_last_error("host all-gather callback failed");
+            return KS_ERR_NCCL;
+        }
+        return KS_OK;
+    }
+    // NCCL moves device memory: stage through a small device buffer
+    void* d = nullptr;
+    ks_status s = cuda_status(cudaMalloc(&d, bytes * c->world));
+    if (s == KS_OK)
+        s = cuda_status(cudaMemcpy(static_cast<char*>(d) + c->rank * bytes, send, bytes, cudaMemcpyHostToDevice));
+    if (s == KS_OK)
+        s = nccl_status(ncclAllGather(static_cast<char*>(d) + c->rank * bytes, d, bytes, ncclUint8, c->nccl, nullptr));
+    if (s == KS_OK) s = cuda_status(cudaStreamSynchronize(nullptr));
+    if (s == KS_OK) s = cuda_status(cudaMemcpy(recv, d, bytes * c->world, cudaMemcpyDeviceToHost));
+    if (d) cudaFree(d);
+    return s;
+}
+
+// Host-communicator all-gather of a device array dk[n] into the device array
+// gather[world, n]: D2H after the stream's prior work, the caller's exchange,
+// H2D back on the stream.
+static ks_status host_gather_device(ks_comm* c, const float* dk, float* gather, size_t n, cudaStream_t st) {
+    std::vector<float> mine(n), all(n * c->world);
+    ks_status s = cuda_status(cudaMemcpyAsync(mine.data(), dk, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+    if (s == KS_OK) s = cuda_status(cudaStreamSynchronize(st));
+    if (s == KS_OK) s = comm_allgather_host(c, mine.data(), all.data(), n * sizeof(float));
+    if (s == KS_OK)
+        s = cuda_status(cudaMemcpyAsync(gather, all.data(), all.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+    if (s == KS_OK) s = cuda_status(cudaStreamSynchronize(st));  // `all` is pageable and goes out of scope
+    return s;
+}
+
 }  // namespace ks
 
 using namespace ks;
@@ -103,10 +147,38 @@ ks_status ks_comm_init(ks_comm** comm, const void* id128, int world, int rank) {
     return KS_OK;
 }
 
+ks_status ks_comm_init_host(ks_comm** comm, int world, int rank, ks_allgather_fn allgather, void* ctx) {
+    if (!comm || !allgather) return KS_ERR_NULL;
+    if (world < 1 || rank < 0 || rank >= world) return KS_ERR_SHARD;
+    ks_comm* c = new ks_comm;
+    c->world = world;
+    c->rank = rank;
+    c->host_allgather = allgather;
+    c->host_ctx = ctx;
+    *comm = c;
+    return KS_OK;
+}
+
+ks_status ks_rank_tree_sum_f32(const float* gather, float* out, int64_t n, int world, void* stream) {
+    if (!gather || !out) return KS_ERR_NULL;
+    if (world < 1 || world > 64) return KS_ERR_SHARD;
+    if (n < 0) return KS_ERR_DIM_H;
+    if (n == 0) return KS_OK;
+    rank_tree_sum<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+        gather, out, n, world);
+    return check_launch();
+}
+
+ks_status ks_comm_allgather_host(ks_comm* comm, const void* send, void* recv, size_t bytes) {
+    if (!comm || (bytes && (!send || !recv))) return KS_ERR_NULL;
+    if (bytes == 0) return KS_OK;
+    return comm_allgather_host(comm, send, recv, bytes);
+}
+
 ks_status ks_comm_destroy(ks_comm* comm) {
     if (!comm) return KS_OK;
     ks_status s = KS_OK;
-    if (comm->nccl) s = nccl_status(ncclCommDestroy(comm->nccl));
+    if (comm->nccl) s = nccl_status(ncclCommDestroy(comm->nccl));  // host communicators own nothing
     delete comm;
     return s;
 }
@@ -116,6 +188,16 @@ ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm*
     if (!dk || !comm) return KS_ERR_NULL;
     if (H < 1) return KS_ERR_DIM_H;
     if (K < 1) return KS_ERR_DIM_K;
+    if (comm->host_allgather) {  // deterministic: gather every rank's dk, fixed tree on the device
+        if (comm->world == 1) return KS_OK;
+        float* gather = nullptr;
+        const size_t n = static_cast<size_t>(H * K);
+        const cudaStream_t st = static_cast<cudaStream_t>(stream);
+        ks_status s = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&gather), n * comm->world * sizeof(float), st));
+        if (s == KS_OK) s = ks_dwconv1d_dw_allgather_sum_f32(dk, gather, H, K, comm, stream);
+        if (gather) cudaFreeAsync(gather, st);
+        return s;
+    }
     // (a 1-rank communicator still goes through NCCL: same code path at every N)
     return nccl_status(ncclAllReduce(dk, dk, static_cast<size_t>(H * K), ncclFloat, ncclSum,
                                      comm->nccl, static_cast<cudaStream_t>(stream)));
@@ -129,12 +211,10 @@ ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, 
     if (comm->world > 64) return KS_ERR_SHARD;
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
     const size_t n = static_cast<size_t>(H * K);
-    ks_status s = nccl_status(ncclAllGather(dk, gather, n, ncclFloat, comm->nccl, st));
+    ks_status s = comm->host_allgather ? host_gather_device(comm, dk, gather, n, st)
+                                       : nccl_status(ncclAllGather(dk, gather, n, ncclFloat, comm->nccl, st));
     if (s != KS_OK) return s;
-    rank_tree_sum<<<static_cast<unsigned>((n + 255) / 256), 256, 0, st>>>(gather, dk,
-                                                                          static_cast<int64_t>(n),
-                                                                          comm->world);
-    return check_launch();
+    return ks_rank_tree_sum_f32(gather, dk, static_cast<int64_t>(n), comm->world, stream);
 }
 
 }  // extern "C"

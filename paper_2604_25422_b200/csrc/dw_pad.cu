@@ -218,6 +218,22 @@ ks_status launch(const CUtensorMap& gm, const CUtensorMap& xm, float* part, int6
 
 }  // namespace
 
+// Envelope of the compute-bound dW kernel (K >= 128, L >= 2048, L % 32 == 0).
+bool dw_pad_applies(int64_t B, int64_t H, int64_t L, int64_t K) {
+    return K >= 128 && K <= 8192 && L >= 2048 && L % 32 == 0 && L < (int64_t(1) << 30) &&
+           B * H < (int64_t(1) << 31);
+}
+
+// Row groups G of dw_pad's partial buffer: enough CTAs to fill the GPU a few
+// times over (G * H * tap tiles ~ 2048).
+int dw_pad_groups(int64_t B, int64_t H, int64_t K) {
+    int njg = 4;
+    while (njg < 32 && njg * kJR < K) njg *= 2;
+    const int64_t njt = (K + njg * kJR - 1) / (njg * kJR);
+    const int64_t G = (2048 + H * njt - 1) / (H * njt);
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(G, B)));
+}
+
 // Compute-bound dW stage 1 from the padded TMA view (K >= 128, L >= 2048,
 // L % 32 == 0), into part[G,H,K].  *handled = false outside the envelope.
 ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
@@ -254,15 +270,10 @@ ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B,
         return KS_OK;
     }
     g.stage_bytes = ((g.gy_alloc + g.nbx * g.NBX) * 144 + 1023) / 1024 * 1024;
-    {
-        const char* e = getenv("KS_PAD_SKIP");
-        g.skip = !(e && *e == '0');
-    }
+    g.skip = opt(kOptPadSkip) != 0;
     int NS = 3;
     while (NS > 2 && dwpad_smem(g, NS) > 110 * 1024) --NS;
-    if (const char* e = getenv("KS_DWPAD_NS")) {  // tuning knob
-        if (atoi(e) > 0) NS = std::min(4, atoi(e));
-    }
+    if (opt(kOptDwpadNs) > 0) NS = static_cast<int>(opt(kOptDwpadNs));  // tuning option
     if (dwpad_smem(g, NS) > 220 * 1024) return KS_OK;
     CUtensorMap gm, xm;
     if (!encode_padded_view(&gm, gy, B * H, L, H, g.gy_rows, 1, 1)) return KS_OK;

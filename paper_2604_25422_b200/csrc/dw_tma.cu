@@ -285,8 +285,7 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
     // (a t-slice must cover a whole 16-wide block of the 2048-wide work item)
     // 8 < K <= 16: one tap group of 16 taps over 8-wide t blocks (16 x 8 FMAs
     // per 2 gy + 6-7 x loads, half the shared traffic of two 8-tap groups)
-    const char* e16 = getenv("KS_DWTMA_J16");  // A/B knob: 0 = two 8-tap groups
-    const bool j16 = K > 8 && K <= 16 && !(e16 && *e16 == '0');
+    const bool j16 = K > 8 && K <= 16 && opt(kOptDwtmaJ16) != 0;  // option 0: two 8-tap groups
     const int JR = K <= 16 && !j16 ? 8 : 16;
     int nj = JR == 8 || j16 ? 1 : 2;
     while (nj < 8 && nj * JR < K) nj *= 2;
@@ -312,9 +311,7 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
     // 3 for K > 8, where a fourth CTA per SM hides more FMA latency
     // (config 5a dW 10.7 -> 10.1 ms, fused backward 22.4 -> 20.4 ms)
     int NS = std::max(2, std::min(K > 8 ? 3 : 4, (72 * 1024) / g.stage_bytes));
-    if (const char* e = getenv("KS_DWTMA_NS")) {  // tuning knob
-        if (atoi(e) >= 1 && atoi(e) <= 6) NS = atoi(e);
-    }
+    if (opt(kOptDwtmaNs) > 0) NS = static_cast<int>(opt(kOptDwtmaNs));  // tuning option
     const int p = static_cast<int>(K / 2);
     const int s = (4 - p % 4) % 4;
     const int q = static_cast<int>(K) - 1 - p;
@@ -346,9 +343,8 @@ ks_status bwd_short_fused_stage1(const float*, const float*, const float*, float
 // instructions) unless an A/B knob asks for this file's generic kernel.
 static bool use_bwd_short(int64_t K) {
     if (K > 16) return false;
-    const char* e = getenv("KS_BWDS");
-    if (e && *e == '0') return false;
-    return !getenv("KS_DWTMA_NS") && !(getenv("KS_DWTMA_J16") && *getenv("KS_DWTMA_J16") == '0');
+    if (opt(kOptBwds) == 0) return false;
+    return opt(kOptDwtmaNs) == 0 && opt(kOptDwtmaJ16) != 0;
 }
 
 // Stage 1 of HIERARCHICAL dW through TMA into part[G,H,K] (G = the caller's row

@@ -23,28 +23,16 @@ namespace {
 
 // target bytes per streamed block (tuning knob KS_HOST_BLOCK_MB)
 size_t block_bytes() {
-    static const size_t b = [] {
-        const char* e = getenv("KS_HOST_BLOCK_MB");
-        const long mb = e ? atol(e) : 64;
-        return size_t(mb >= 1 && mb <= 4096 ? mb : 64) << 20;
-    }();
-    return b;
+    return size_t(opt(kOptHostBlockMb)) << 20;
 }
 constexpr int kSlots = 3;
 
-struct DevicePool {
-    DevicePool() {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = ~0ull;  // keep freed blocks cached between calls
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
-    }
-};
-
-void ensure_pool() { static DevicePool p; }
+// Device buffers come from the library's own stream-ordered pool (capi.cu),
+// never the process-wide default pool, whose settings belong to the caller.
+template <typename T>
+cudaError_t scratch_alloc_t(T** p, size_t bytes, cudaStream_t st) {
+    return scratch_alloc(reinterpret_cast<void**>(p), bytes, st);
+}
 
 template <typename T>
 using StencilFn = ks_status (*)(const T*, const T*, T*, int64_t, int64_t, int64_t, int64_t, int,
@@ -54,7 +42,6 @@ template <typename T>
 ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t B, int64_t H,
                        int64_t L, int64_t K, int mode) {
     if (!in || !k || !out) return KS_ERR_NULL;
-    ensure_pool();
     const size_t entry = sizeof(T) * size_t(H) * size_t(L);  // one batch entry
     const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(block_bytes() / std::max<size_t>(entry, 1))));
     const int64_t nblocks = (B + nb - 1) / nb;
@@ -67,7 +54,7 @@ ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t
     ks_status rc = KS_OK;
     for (int s = 0; s < slots && rc == KS_OK; ++s)
         rc = cuda_status(cudaStreamCreateWithFlags(&st[s], cudaStreamNonBlocking));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dk, sizeof(T) * H * K, st[0]));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dk, sizeof(T) * H * K, st[0]));
     if (rc == KS_OK)
         rc = cuda_status(cudaMemcpyAsync(dk, k, sizeof(T) * H * K, cudaMemcpyHostToDevice, st[0]));
     cudaEvent_t k_ready = nullptr;
@@ -75,8 +62,8 @@ ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t
     if (rc == KS_OK) rc = cuda_status(cudaEventRecord(k_ready, st[0]));
     for (int s = 0; s < slots && rc == KS_OK; ++s) {
         if (s) rc = cuda_status(cudaStreamWaitEvent(st[s], k_ready, 0));
-        if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&din[s], entry * nb, st[s]));
-        if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dout[s], entry * nb, st[s]));
+        if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&din[s], entry * nb, st[s]));
+        if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dout[s], entry * nb, st[s]));
     }
     for (int64_t i = 0; i < nblocks && rc == KS_OK; ++i) {
         const int s = static_cast<int>(i % slots);
@@ -90,8 +77,8 @@ ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t
     }
     for (int s = 0; s < slots; ++s) {
         if (!st[s]) continue;
-        if (din[s]) cudaFreeAsync(din[s], st[s]);
-        if (dout[s]) cudaFreeAsync(dout[s], st[s]);
+        if (din[s]) scratch_free(din[s], st[s]);
+        if (dout[s]) scratch_free(dout[s], st[s]);
     }
     if (dk && st[0]) {
         for (int s = 1; s < slots; ++s) {
@@ -102,7 +89,7 @@ ks_status stencil_host(StencilFn<T> fn, const T* in, const T* k, T* out, int64_t
                 cudaEventDestroy(e);
             }
         }
-        cudaFreeAsync(dk, st[0]);
+        scratch_free(dk, st[0]);
     }
     for (int s = 0; s < slots; ++s) {
         if (!st[s]) continue;
@@ -122,7 +109,6 @@ template <typename T>
 ks_status dw_host(DwFn<T> fn, const T* gy, const T* x, T* dk, int64_t B, int64_t H, int64_t L,
                   int64_t K, int scheme, int64_t chunk, int mode) {
     if (!gy || !x || !dk) return KS_ERR_NULL;
-    ensure_pool();
     const size_t tbytes = sizeof(T) * size_t(B) * size_t(H) * size_t(L);
     cudaStream_t s0 = nullptr, s1 = nullptr;
     T *dgy = nullptr, *dx = nullptr, *ddk = nullptr;
@@ -130,9 +116,9 @@ ks_status dw_host(DwFn<T> fn, const T* gy, const T* x, T* dk, int64_t B, int64_t
     ks_status rc = cuda_status(cudaStreamCreateWithFlags(&s0, cudaStreamNonBlocking));
     if (rc == KS_OK) rc = cuda_status(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
     if (rc == KS_OK) rc = cuda_status(cudaEventCreateWithFlags(&x_ready, cudaEventDisableTiming));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dgy, tbytes, s0));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dx, tbytes, s1));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&ddk, sizeof(T) * H * K, s0));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dgy, tbytes, s0));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dx, tbytes, s1));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&ddk, sizeof(T) * H * K, s0));
     if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dgy, gy, tbytes, cudaMemcpyHostToDevice, s0));
     if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dx, x, tbytes, cudaMemcpyHostToDevice, s1));
     if (rc == KS_OK) rc = cuda_status(cudaEventRecord(x_ready, s1));
@@ -145,9 +131,9 @@ ks_status dw_host(DwFn<T> fn, const T* gy, const T* x, T* dk, int64_t B, int64_t
         cudaStreamWaitEvent(s0, x_ready, 0);
     }
     if (s0) {
-        if (dgy) cudaFreeAsync(dgy, s0);
-        if (dx) cudaFreeAsync(dx, s0);
-        if (ddk) cudaFreeAsync(ddk, s0);
+        if (dgy) scratch_free(dgy, s0);
+        if (dx) scratch_free(dx, s0);
+        if (ddk) scratch_free(ddk, s0);
         const ks_status e = cuda_status(cudaStreamSynchronize(s0));
         if (rc == KS_OK) rc = e;
         cudaStreamDestroy(s0);
@@ -169,7 +155,6 @@ ks_status dw_host(DwFn<T> fn, const T* gy, const T* x, T* dk, int64_t B, int64_t
 ks_status step_host(const float* x, const float* k, const float* gy, float* y, float* dxo, float* dk, int64_t B,
                     int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk, int mode) {
     if (!x || !k || !gy || !y || !dxo || !dk) return KS_ERR_NULL;
-    ensure_pool();
     const size_t entry = sizeof(float) * size_t(H) * size_t(L);
     const size_t tbytes = entry * size_t(B);
     const int64_t nb = std::max<int64_t>(1, std::min<int64_t>(B, int64_t(block_bytes() / std::max<size_t>(entry, 1))));
@@ -189,13 +174,13 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
         if (rc == KS_OK) rc = cuda_status(cudaEventCreateWithFlags(&up[s], cudaEventDisableTiming));
     }
     if (rc == KS_OK) rc = cuda_status(cudaStreamCreateWithFlags(&sdw, cudaStreamNonBlocking));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dxin, tbytes, st[0]));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dgy, tbytes, st[0]));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&dkk, sizeof(float) * H * K, st[0]));
-    if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&ddk, sizeof(float) * H * K, st[0]));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dxin, tbytes, st[0]));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dgy, tbytes, st[0]));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&dkk, sizeof(float) * H * K, st[0]));
+    if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&ddk, sizeof(float) * H * K, st[0]));
     for (int s = 0; s < slots && rc == KS_OK; ++s) {
-        rc = cuda_status(cudaMallocAsync(&dy[s], entry * nb, st[0]));
-        if (rc == KS_OK) rc = cuda_status(cudaMallocAsync(&ddx[s], entry * nb, st[0]));
+        rc = cuda_status(scratch_alloc_t(&dy[s], entry * nb, st[0]));
+        if (rc == KS_OK) rc = cuda_status(scratch_alloc_t(&ddx[s], entry * nb, st[0]));
     }
     if (rc == KS_OK) rc = cuda_status(cudaMemcpyAsync(dkk, k, sizeof(float) * H * K, cudaMemcpyHostToDevice, st[0]));
     if (rc == KS_OK) rc = cuda_status(cudaEventRecord(ev[0], st[0]));
@@ -225,13 +210,13 @@ ks_status step_host(const float* x, const float* k, const float* gy, float* y, f
     for (int s = 0; s < slots; ++s)
         if (st[s]) cudaStreamSynchronize(st[s]);
     if (st[0]) {
-        if (dxin) cudaFreeAsync(dxin, st[0]);
-        if (dgy) cudaFreeAsync(dgy, st[0]);
-        if (dkk) cudaFreeAsync(dkk, st[0]);
-        if (ddk) cudaFreeAsync(ddk, st[0]);
+        if (dxin) scratch_free(dxin, st[0]);
+        if (dgy) scratch_free(dgy, st[0]);
+        if (dkk) scratch_free(dkk, st[0]);
+        if (ddk) scratch_free(ddk, st[0]);
         for (int s = 0; s < slots; ++s) {
-            if (dy[s]) cudaFreeAsync(dy[s], st[0]);
-            if (ddx[s]) cudaFreeAsync(ddx[s], st[0]);
+            if (dy[s]) scratch_free(dy[s], st[0]);
+            if (ddx[s]) scratch_free(ddx[s], st[0]);
         }
         const ks_status e = cuda_status(cudaStreamSynchronize(st[0]));
         if (rc == KS_OK) rc = e;

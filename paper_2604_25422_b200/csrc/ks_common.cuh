@@ -42,13 +42,12 @@ __device__ __forceinline__ void st_cs_v4(float* p, float4 v) {
 }
 
 inline int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
+    static const int n = [] {  // thread-safe static init
+        int dev = 0, v = 0;
         cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 148;
+    }();
     return n;
 }
 
@@ -66,6 +65,32 @@ int prepare_kernel(const void* func, int threads, int smem);
 
 // Records a CUDA error for ks_last_error_string and maps it to a status.
 ks_status cuda_status(cudaError_t e);
+// Called after every kernel launch of the library: maps a launch error to a
+// status and counts the launch (ks_launch_count).
 ks_status check_launch();
+void set_last_error(const char* what);
+
+// Tuning options (options.cu; ks_set_option).  Order = the table in options.cu.
+enum Opt {
+    kOptDisableTma = 0,
+    kOptLdg,
+    kOptSts,
+    kOptBwds,
+    kOptDst,
+    kOptDwtmaJ16,
+    kOptDwtmaNs,
+    kOptPadSkip,
+    kOptPadNs,
+    kOptPadProd,
+    kOptDwpadNs,
+    kOptStencilPad,
+    kOptStencilR,
+    kOptStencilNt,
+    kOptStencilNs,
+    kOptHostBlockMb,
+    kOptCount
+};
+int64_t opt(Opt o);
+inline bool tma_disabled() { return opt(kOptDisableTma) != 0; }
 
 }  // namespace ks

@@ -121,8 +121,7 @@ ks_status launch_any(int64_t K, bool fused, const float* in, const float4* kp, f
 ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
                           int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
-    const char* e = getenv("KS_LDG");
-    const int knob = e && *e ? atoi(e) : 1;
+    const int knob = static_cast<int>(opt(kOptLdg));
     if (knob == 0 || K > (knob >= 2 ? 16 : 8)) return KS_OK;
     if (K < 1 || K > 16 || L % 8 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;

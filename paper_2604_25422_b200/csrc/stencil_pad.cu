@@ -281,10 +281,6 @@ ks_status launch_s(int s, bool fused, const CUtensorMap& im, const float* kp, fl
     }
 }
 
-int env_knob(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
 
 }  // namespace
 
@@ -306,7 +302,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.base_row = static_cast<int>((off + lead) / 32);
     g.off = static_cast<int>(off);
     g.zlead = zlead;
-    g.skip = env_knob("KS_PAD_SKIP", 1) != 0;
+    g.skip = opt(kOptPadSkip) != 0;
     g.RPT = 1;
     while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
     g.TPR = NT / g.RPT;
@@ -328,7 +324,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     // per SM stays >= 2; long K (>= 1024) computes ~100x longer than it loads
     int NS = K >= 1024 ? 1 : 3;
     while (NS > 1 && pad_smem(g, NS) > 110 * 1024) --NS;
-    if (env_knob("KS_PAD_NS", 0) > 0) NS = std::min(4, env_knob("KS_PAD_NS", 0));
+    if (opt(kOptPadNs) > 0) NS = static_cast<int>(std::min<int64_t>(4, opt(kOptPadNs)));
     if (pad_smem(g, NS) > 220 * 1024) return KS_OK;
     CUtensorMap im;
     if (!encode_padded_view(&im, in, B * H, L, H, g.NB, g.RPT, 1)) return KS_OK;
@@ -342,7 +338,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;
         // long K: one stage, refilled after a CTA barrier; moderate K: producer lane
-        const bool prod = env_knob("KS_PAD_PROD", K >= 1024 ? 0 : 1) != 0;
+        const bool prod = opt(kOptPadProd) < 0 ? K < 1024 : opt(kOptPadProd) != 0;
         rc = prod ? launch_s<true>(S, fused, im, kp, out, B, H, L, g, NS, st)
                   : launch_s<false>(S, fused, im, kp, out, B, H, L, g, NS, st);
     }

@@ -29,8 +29,6 @@
 namespace ks {
 
 __global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
-ks_status stencil_cb_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
-                         int64_t off, int reverse, int mode, cudaStream_t st, bool* handled);
 ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B, int64_t H, int64_t L, int64_t K,
                           int64_t off, int reverse, int mode, cudaStream_t st, bool* handled);
 
@@ -222,11 +220,6 @@ ks_status launch_s(int s, bool fused, const CUtensorMap& im, const CUtensorMap& 
 
 }  // namespace
 
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v && *v ? atoi(v) : dflt;
-}
-
 // Register-tile shape for (L, K): R = 32 for compute-bound long K, R = 16 for
 // memory-bound short K, R = 4 for short rows; NT chosen so a tile (NT*R
 // outputs) does not exceed the row.
@@ -255,25 +248,22 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     *handled = false;
     if (L % kIn != 0 || L >= (int64_t(1) << 30) || K > 8192) return KS_OK;
     if ((reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
-    if (env_int("KS_STENCIL_CB", 1)) {  // compute-bound long-K kernels
-        // padded TMA view (stencil_pad.cu); KS_CB_IMPL=1 selects stencil_cb.cu (A/B knob)
-        const ks_status s = env_int("KS_CB_IMPL", 0) == 1
-                                ? stencil_cb_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled)
-                                : stencil_pad_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
+    if (opt(kOptStencilPad)) {  // compute-bound long-K kernels from the padded TMA view (stencil_pad.cu)
+        const ks_status s = stencil_pad_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }
-    if (K <= 16 && L >= 1024 && env_int("KS_STS", 1)) {  // K-specialised short-kernel stencil (bwd_short.cuh)
+    if (K <= 16 && L >= 1024 && opt(kOptSts)) {  // K-specialised short-kernel stencil (bwd_short.cuh)
         const ks_status s = stencil_short_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }
     int R, NT;
     pick_tile(L, K, &R, &NT);
-    if (env_int("KS_STENCIL_R", 0) == 32 && L >= 2048) {  // tuning knob: R = 32 register tiles at short K
+    if (opt(kOptStencilR) == 32 && L >= 2048) {  // tuning option: R = 32 register tiles at short K
         R = 32;
         NT = L >= 8192 ? 256 : L >= 4096 ? 128 : 64;
     }
-    if (R == 16 && env_int("KS_STENCIL_NT", 0) > 0) {  // tuning knob (bench sweeps)
-        const int nt = env_int("KS_STENCIL_NT", 0);
+    if (R == 16 && opt(kOptStencilNt) > 0) {  // tuning option (bench sweeps)
+        const int nt = static_cast<int>(opt(kOptStencilNt));
         if ((nt == 64 || nt == 128 || nt == 256) && nt * R <= L) NT = nt;
     }
     const bool tma_out = R != 32;
@@ -317,7 +307,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
         // load by ~100x and one stage suffices; shorter K keeps one tile in flight.
         NS = K >= 1024 ? 1 : 2;
     }
-    if (env_int("KS_STENCIL_NS", 0) > 0) NS = std::min(8, env_int("KS_STENCIL_NS", 0));  // tuning knob
+    if (opt(kOptStencilNs) > 0) NS = static_cast<int>(opt(kOptStencilNs));  // tuning option
     if (stencil_smem_bytes(g, NS, tma_out) > 220 * 1024) return KS_OK;
 
     float* kp = nullptr;

@@ -25,7 +25,7 @@ def test_library_exports_every_declared_symbol():
     for name in declared:
         assert hasattr(lib, name), name
     assert set(declared) == set(_lib.EXPORTED)
-    assert lib.ks_abi_version() == 1
+    assert lib.ks_abi_version() == 2
     assert lib.ks_status_string(0) == b"ok"
 
 
@@ -98,3 +98,47 @@ def test_shard_rows_cover_batch():
             assert max(n for _, n in spans) - min(n for _, n in spans) <= 1
     with pytest.raises(ks.KsError):
         ks.shard_rows(4, 8, 0)
+
+
+def test_tuning_options_are_explicit_and_validated():
+    """Tier switches are an explicit, validated API (ks_set_option): no
+    environment variable changes what the library runs."""
+    import paper_2604_25422_b200 as ks
+    assert ks.get_option("ldg") == 1 and ks.get_option("bwds") == 1 and ks.get_option("disable_tma") == 0
+    with ks.options(ldg=2, bwds=0):
+        assert ks.get_option("ldg") == 2 and ks.get_option("bwds") == 0
+    assert ks.get_option("ldg") == 1 and ks.get_option("bwds") == 1
+    with pytest.raises(ks.KsError, match="BAD_OPTION"):
+        ks.set_option("ldg", 9)
+    with pytest.raises(ks.KsError, match="BAD_OPTION"):
+        ks.set_option("no_such_option", 1)
+    ks.set_option("pad_prod", 0)
+    ks.set_option("pad_prod")  # back to the default
+    assert ks.get_option("pad_prod") == -1
+    import subprocess
+    import sys
+    code = ("import paper_2604_25422_b200 as ks; print(ks.get_option('ldg'), ks.get_option('disable_tma'))")
+    env = dict(os.environ, KS_LDG="0", KS_DISABLE_TMA="1")
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True, text=True)
+    assert out.stdout.split() == ["1", "0"], out.stdout + out.stderr
+
+
+def test_python_mirror_checks_outputs_before_the_c_abi():
+    """Outputs, kernels and workspaces of the wrong kind / dtype / shape are
+    rejected in Python: the C ABI takes raw pointers and would otherwise
+    write out of bounds or dereference a host pointer on the device."""
+    import paper_2604_25422_b200 as ks
+    x = np.zeros((2, 3, 16), np.float32)
+    k = np.zeros((3, 5), np.float32)
+    with pytest.raises(ks.DimensionError, match="out"):
+        ks.forward(x, k, out=np.zeros((2, 3, 15), np.float32))
+    with pytest.raises(TypeError, match="dtype"):
+        ks.forward(x, k, out=np.zeros((2, 3, 16), np.float64))
+    with pytest.raises(TypeError, match="dtype"):
+        ks.forward(x, k.astype(np.float64))
+    with pytest.raises(ks.DimensionError, match="out"):
+        ks.backward_weight(x, x, 5, ks.HIERARCHICAL, out=np.zeros((3, 4), np.float32))
+    torch = pytest.importorskip("torch")
+    with pytest.raises(TypeError, match="numpy"):
+        ks.forward(x, torch.zeros((3, 5)))
+

@@ -37,6 +37,46 @@ def rank_tree(vals):
     return (rank_tree(vals[:mid]) + rank_tree(vals[mid:])).astype(np.float32)
 
 
+def _entry(rank, world, port, fn, results, args):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fn(rank, world, results, *args)
+    finally:
+        dist.destroy_process_group()
+
+
+def run_world(world, fn, *args):
+    """Run fn(rank, world, results, *args) on `world` processes joined by a
+    gloo group (127.0.0.1); returns the shared results dict."""
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_entry, args=(world, _free_port(), fn, results, args), nprocs=world, join=True)
+    return dict(results)
+
+
+def gloo_allgather(data: bytes):
+    """A host all-gather over the default (gloo) group: the transport handed
+    to the library's ks_comm_init_host."""
+    t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [o.numpy().tobytes() for o in out]
+
+
+def host_comm_worker(rank, world, results):
+    """The library's host communicator on CPU: rank-ordered all-gather of
+    uneven payloads' fixed-size records through the caller's gloo transport."""
+    import paper_2604_25422_b200 as ks
+    comm = ks.Comm.host(world, rank, gloo_allgather)
+    try:
+        got = comm.allgather_bytes(bytes([rank]) * 5 + rank.to_bytes(4, "little"))
+        results[rank] = got
+    finally:
+        comm.close()
+    assert got == [bytes([r]) * 5 + r.to_bytes(4, "little") for r in range(world)]
+
+
 def _worker(rank, world, port, results):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -86,3 +126,12 @@ def test_batch_sharded_step_world2(world):
     full = o.backward_weight(gy, x, K, PAIRWISE)
     assert np.array_equal(results["exact"].view(np.uint32), full.view(np.uint32))
     assert normwise(results["allreduce"], full) <= 1e-6
+
+
+def test_host_communicator_world2_gloo():
+    """ks_comm_init_host over a torch.distributed gloo all-gather, world size
+    2 (CPU): the library's own communicator moves every rank's bytes in rank
+    order -- the transport the multi-rank dW combines use when ranks share a
+    GPU (tests/test_multirank_gpu.py runs those on the B200)."""
+    res = run_world(2, host_comm_worker)
+    assert res[0] == res[1]
