@@ -152,6 +152,23 @@ ks_status ks_launch_count(uint64_t* count);
 ks_status ks_set_option(const char* name, int64_t value);
 ks_status ks_get_option(const char* name, int64_t* value);
 
+/* The launch plan of one entry point for a shape -- this library's
+ * counterpart of the reference's launch_geometry / shared_mem_footprint
+ * (proj/include/kernelscope/exec_model.hpp:14-127), produced by the real
+ * dispatch code run without launching: every kernel the call would launch, in
+ * order, with its grid, block and dynamic shared memory.  path: 0 forward,
+ * 1 dX, 2 dW (scheme, chunk as ks_dwconv1d_dw_f32), 3 the layer backward
+ * (ks_dwconv1d_bwd_f32).  Operands are taken as 16-byte aligned.  *n = the
+ * number of launches (records beyond `cap` are not written).  Needs a
+ * device (occupancy and tensor-map queries); no device memory is touched. */
+typedef struct ks_launch_rec {
+    char kernel[256]; /* demangled kernel signature */
+    uint32_t grid[3], block[3];
+    uint64_t smem_bytes; /* dynamic shared memory */
+} ks_launch_rec;
+ks_status ks_dwconv1d_plan(int path, int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                           int mode, ks_launch_rec* recs, int cap, int* n);
+
 /* Measured FP32 FMA throughput of the current device (TFLOP/s, 2 FLOP per
  * FMA): the compute roof for the long-K (FP32-bound) shapes.  Synchronous. */
 ks_status ks_probe_fp32_tflops(double* tflops);

@@ -31,7 +31,7 @@ EXPORTED = [
     "ks_status_string", "ks_last_error_string", "ks_abi_version",
     "ks_dwconv1d_fwd_f32", "ks_dwconv1d_fwd_f64", "ks_dwconv1d_dx_f32", "ks_dwconv1d_dx_f64",
     "ks_dwconv1d_dw_workspace_bytes", "ks_dwconv1d_dw_f32", "ks_dwconv1d_dw_f64",
-    "ks_dwconv1d_bwd_f32", "ks_fill_pm1_f32", "ks_launch_count", "ks_set_option", "ks_get_option",
+    "ks_dwconv1d_bwd_f32", "ks_fill_pm1_f32", "ks_launch_count", "ks_dwconv1d_plan", "ks_set_option", "ks_get_option",
     "ks_probe_fp32_tflops",
     "ks_dwconv1d_fwd_f32_host", "ks_dwconv1d_dx_f32_host", "ks_dwconv1d_dw_f32_host",
     "ks_dwconv1d_fwd_f64_host", "ks_dwconv1d_dx_f64_host", "ks_dwconv1d_dw_f64_host",
@@ -61,6 +61,7 @@ _SIGS = {
     "ks_fill_pm1_f32": ([_u64, _u64, _p, _i64, _p], _int),
     "ks_probe_fp32_tflops": ([C.POINTER(C.c_double)], _int),
     "ks_launch_count": ([C.POINTER(_u64)], _int),
+    "ks_dwconv1d_plan": ([_int, _i64, _i64, _i64, _i64, _int, _i64, _int, _p, _int, C.POINTER(_int)], _int),
     "ks_set_option": ([C.c_char_p, _i64], _int),
     "ks_get_option": ([C.c_char_p, C.POINTER(_i64)], _int),
     "ks_dwconv1d_fwd_f32_host": ([_p, _p, _p, _i64, _i64, _i64, _i64, _int], _int),
@@ -86,6 +87,14 @@ _SIGS = {
     "ks_dwconv1d_dw_f32_peer": ([_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _int, _p, _p], _int),
     "ks_peer_timed_out": ([_p, C.POINTER(_int)], _int),
 }
+
+
+
+class LaunchRec(C.Structure):
+    """ks_launch_rec (include/ks_dwconv1d.h)."""
+    _fields_ = [("kernel", C.c_char * 256), ("grid", C.c_uint32 * 3), ("block", C.c_uint32 * 3),
+                ("smem_bytes", C.c_uint64)]
+
 
 _lib = None
 

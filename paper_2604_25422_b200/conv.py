@@ -470,3 +470,22 @@ def launch_count() -> int:
     v = C.c_uint64(0)
     check(_lib.lib().ks_launch_count(C.byref(v)), "launch_count")
     return int(v.value)
+
+
+PLAN_PATHS = {"fwd": 0, "dx": 1, "dw": 2, "bwd": 3}
+
+
+def plan(path: str, B: int, H: int, L: int, K: int, scheme: int = HIERARCHICAL, chunk: int = 0,
+         mode: int = SEPARATE) -> list:
+    """ks_dwconv1d_plan: the kernels one call would launch for this shape
+    (kernel, grid, block, dynamic smem) -- the real dispatch run without
+    launching; this library's launch_geometry / shared_mem_footprint
+    (reference proj/include/kernelscope/exec_model.hpp:14-127).  Needs a device."""
+    cap = 64
+    recs = (_lib.LaunchRec * cap)()
+    n = C.c_int(0)
+    st = _lib.lib().ks_dwconv1d_plan(PLAN_PATHS[path], B, H, L, K, scheme, chunk, mode, C.addressof(recs), cap,
+                                     C.byref(n))
+    _raise_dims(st, f"plan {path}")
+    return [{"kernel": r.kernel.decode(), "grid": tuple(r.grid), "block": tuple(r.block),
+             "smem": int(r.smem_bytes)} for r in recs[:min(n.value, cap)]]

@@ -18,7 +18,7 @@ static ks_status launch_stencil_short(const float* in, const float* k, float* ou
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * 16, st));
     if (rc != KS_OK) return rc;
     *handled = true;
-    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st>>>(k, kp, H, K, 16,
+    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st, k, kp, H, K, 16,
                                                                                                    reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {

@@ -2,7 +2,10 @@
 // argument validation in the reference's order (ConvShape ctor checks B,H,L,K,
 // shape.hpp:27-31; chunk_size >= 1, src/conv_core.cpp:154-156), launch
 // selection, scratch management and the on-device splitmix64 generator.
+#include <cxxabi.h>
+
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -42,9 +45,25 @@ ks_status cuda_status(cudaError_t e) {
 
 static std::atomic<uint64_t> g_launches{0};
 
-ks_status check_launch() {
+ks_status check_launch() { return cuda_status(cudaGetLastError()); }
+
+// ---- launch accounting and planning ---------------------------------------
+struct PlanRec {
+    const void* fn;
+    dim3 grid, block;
+    size_t smem;
+};
+static thread_local std::vector<PlanRec>* g_plan = nullptr;
+
+bool planning() { return g_plan != nullptr; }
+
+bool note_launch(const void* fn, dim3 grid, dim3 block, size_t smem) {
+    if (g_plan) {
+        g_plan->push_back({fn, grid, block, smem});
+        return false;
+    }
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cuda_status(cudaGetLastError());
+    return true;
 }
 
 // One library-owned pool per device, created once under a lock (concurrent
@@ -73,12 +92,21 @@ static cudaMemPool_t scratch_pool() {
     return pools[dev];
 }
 
+// While planning, scratch is a placeholder address (aligned, never touched).
+static char* const kPlanScratch = reinterpret_cast<char*>(uintptr_t(0x7e0000000000ull));
+
 cudaError_t scratch_alloc(void** p, size_t bytes, cudaStream_t st) {
+    if (planning()) {
+        *p = kPlanScratch;
+        return cudaSuccess;
+    }
     cudaMemPool_t pool = scratch_pool();
     return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
 }
 
-void scratch_free(void* p, cudaStream_t st) { cudaFreeAsync(p, st); }
+void scratch_free(void* p, cudaStream_t st) {
+    if (!planning()) cudaFreeAsync(p, st);
+}
 
 int prepare_kernel(const void* func, int threads, int smem) {
     // The dynamic-smem opt-in is per (kernel, device) and only ever raised, so a
@@ -369,9 +397,9 @@ ks_status ks_probe_fp32_tflops(double* tflops) {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    fp32_peak_probe<<<blocks, 256>>>(out, 64, 0.999f, 1e-4f);  // warm-up (clocks up)
+    launch_kernel(fp32_peak_probe, blocks, 256, 0, nullptr, out, 64, 0.999f, 1e-4f);  // warm-up (clocks up)
     cudaEventRecord(a);
-    fp32_peak_probe<<<blocks, 256>>>(out, iters, 0.999f, 1e-4f);
+    launch_kernel(fp32_peak_probe, blocks, 256, 0, nullptr, out, iters, 0.999f, 1e-4f);
     cudaEventRecord(b);
     ks_status s = cuda_status(cudaEventSynchronize(b));
     float ms = 0.f;
@@ -385,6 +413,54 @@ ks_status ks_probe_fp32_tflops(double* tflops) {
     return KS_OK;
 }
 
+ks_status ks_dwconv1d_plan(int path, int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
+                           int mode, ks_launch_rec* recs, int cap, int* n) {
+    if (!n || (cap > 0 && !recs)) return KS_ERR_NULL;
+    if (path < 0 || path > 3) return KS_ERR_BAD_SCHEME;
+    KS_TRY(check_shape(B, H, L, K));
+    KS_TRY(check_mode(mode));
+    if (path == 2) KS_TRY(check_dw(scheme, chunk));
+    KS_TRY(check_device());
+    // placeholder operands: 1 KiB aligned, never dereferenced (nothing launches)
+    auto fake = [](int i) { return reinterpret_cast<float*>(uintptr_t(0x7f0000000000ull) + (uintptr_t(i) << 36)); };
+    float *a = fake(0), *b = fake(1), *c = fake(2), *d = fake(3), *e = fake(4);
+    std::vector<PlanRec> recs_v;
+    g_plan = &recs_v;
+    ks_status s = KS_OK;
+    const cudaStream_t st = nullptr;
+    switch (path) {
+        case 0: s = conv_stencil_f32(a, b, c, B, H, L, K, K / 2, 0, mode, st); break;
+        case 1: s = conv_stencil_f32(a, b, c, B, H, L, K, K - 1 - K / 2, 1, mode, st); break;
+        case 2: s = dw_f32(a, b, c, B, H, L, K, scheme, chunk, mode, d, st); break;
+        default: {
+            bool fused = false;
+            s = bwd_fused_f32(a, b, c, d, e, B, H, L, K, mode, fake(5), st, &fused);
+            if (s == KS_OK && !fused) s = conv_stencil_f32(a, c, d, B, H, L, K, K - 1 - K / 2, 1, mode, st);
+            if (s == KS_OK && !fused) s = dw_f32(a, b, e, B, H, L, K, KS_DW_HIERARCHICAL, 0, mode, fake(5), st);
+        }
+    }
+    g_plan = nullptr;
+    if (s != KS_OK) return s;
+    *n = static_cast<int>(recs_v.size());
+    for (int i = 0; i < *n && i < cap; ++i) {
+        ks_launch_rec& r = recs[i];
+        memset(&r, 0, sizeof(r));
+        const char* mangled = nullptr;
+        if (cudaFuncGetName(&mangled, recs_v[i].fn) != cudaSuccess || !mangled) {
+            cudaGetLastError();
+            mangled = "?";
+        }
+        int dst = 0;
+        char* dem = abi::__cxa_demangle(mangled, nullptr, nullptr, &dst);
+        strncpy(r.kernel, dst == 0 && dem ? dem : mangled, sizeof(r.kernel) - 1);
+        free(dem);
+        r.grid[0] = recs_v[i].grid.x, r.grid[1] = recs_v[i].grid.y, r.grid[2] = recs_v[i].grid.z;
+        r.block[0] = recs_v[i].block.x, r.block[1] = recs_v[i].block.y, r.block[2] = recs_v[i].block.z;
+        r.smem_bytes = recs_v[i].smem;
+    }
+    return KS_OK;
+}
+
 ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, void* stream) {
     if (n < 0) return KS_ERR_DIM_L;
     if (n == 0) return KS_OK;
@@ -392,7 +468,7 @@ ks_status ks_fill_pm1_f32(uint64_t seed, uint64_t first, float* out, int64_t n, 
     KS_TRY(check_device());
     const int64_t want = (n + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(want < int64_t(num_sms()) * 64 ? want : int64_t(num_sms()) * 64);
-    fill_pm1_kernel<<<blocks, 256, 0, static_cast<cudaStream_t>(stream)>>>(seed, first, out, n);
+    launch_kernel(fill_pm1_kernel, blocks, 256, 0, static_cast<cudaStream_t>(stream), seed, first, out, n);
     return check_launch();
 }
 

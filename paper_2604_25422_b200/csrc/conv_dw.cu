@@ -385,7 +385,7 @@ ks_status launch_hier_s(int s, const float* gy, const float* x, float* part, int
     const int p = static_cast<int>(K / 2);
 #define KS_HIER_CASE(SV)                                                                  \
     case SV:                                                                              \
-        dw_hier_stage1<NJ, SV, FUSED><<<blocks, kDwThreads, 0, st>>>(                     \
+        launch_kernel(dw_hier_stage1<NJ, SV, FUSED>, blocks, kDwThreads, 0, st,                      \
             gy, x, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L),   \
             static_cast<int>(K), p, pl.g, pl.njt);                                        \
         break;
@@ -451,7 +451,7 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
         const int64_t n = B * L;
         int D = 0;
         while (D < 8 && (int64_t(2) << D) <= n) ++D;
-        dw_pairwise_exact<T><<<static_cast<unsigned>(HK), 256, 0, st>>>(gy, x, dk, B, H, L, K, D);
+        launch_kernel(dw_pairwise_exact<T>, static_cast<unsigned>(HK), 256, 0, st, gy, x, dk, B, H, L, K, D);
         return check_launch();
     }
     const int64_t nc = chunk_count(B, L, scheme, chunk);
@@ -462,21 +462,21 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
         const unsigned blocks =
             static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms()) * 64));
         if (mode == KS_MULADD_FUSED)
-            dw_chunk_partials<T, true><<<blocks, 256, 0, st>>>(gy, x, part, B, H, L, K,
+            launch_kernel(dw_chunk_partials<T, true>, blocks, 256, 0, st, gy, x, part, B, H, L, K,
                                                                nc == 1 ? B * L : chunk, nc);
         else
-            dw_chunk_partials<T, false><<<blocks, 256, 0, st>>>(gy, x, part, B, H, L, K,
+            launch_kernel(dw_chunk_partials<T, false>, blocks, 256, 0, st, gy, x, part, B, H, L, K,
                                                                 nc == 1 ? B * L : chunk, nc);
         ks_status s = check_launch();
         if (s != KS_OK) return s;
-        dw_chunk_total<T><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, nc);
+        launch_kernel(dw_chunk_total<T>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, nc);
         return check_launch();
     }
     const unsigned blocks = static_cast<unsigned>((HK + 127) / 128);
     if (mode == KS_MULADD_FUSED)
-        dw_chunked_fused<T, true><<<blocks, 128, 0, st>>>(gy, x, dk, B, H, L, K, chunk, nc);
+        launch_kernel(dw_chunked_fused<T, true>, blocks, 128, 0, st, gy, x, dk, B, H, L, K, chunk, nc);
     else
-        dw_chunked_fused<T, false><<<blocks, 128, 0, st>>>(gy, x, dk, B, H, L, K, chunk, nc);
+        launch_kernel(dw_chunked_fused<T, false>, blocks, 128, 0, st, gy, x, dk, B, H, L, K, chunk, nc);
     return check_launch();
 }
 
@@ -504,7 +504,7 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
     ks_status s = dw_stage1_only(gy, x, part, B, H, L, K, mode, 0, &G, st);
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
-    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, G);
+    launch_kernel(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, G);
     return check_launch();
 }
 
@@ -530,8 +530,10 @@ ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B
         float* a = nullptr;
         ks_status s = cuda_status(scratch_alloc(reinterpret_cast<void**>(&a), 2 * n * sizeof(float), st));
         if (s != KS_OK) return s;
-        s = cuda_status(cudaMemcpyAsync(a, gy, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
-        if (s == KS_OK) s = cuda_status(cudaMemcpyAsync(a + n, x, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        if (!planning()) {
+            s = cuda_status(cudaMemcpyAsync(a, gy, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+            if (s == KS_OK) s = cuda_status(cudaMemcpyAsync(a + n, x, n * sizeof(float), cudaMemcpyDeviceToDevice, st));
+        }
         if (s == KS_OK) s = dw_stage1_only(a, a + n, part, B, H, L, K, mode, G_req, G, st);
         scratch_free(a, st);
         return s;
@@ -573,7 +575,7 @@ ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* 
     const ks_status s = bwd_tma_stage1(gy, x, k, dx, part, B, H, L, K, pl.g, mode, st, fused);
     if (s != KS_OK || !*fused) return s;
     const int64_t HK = H * K;
-    dw_sum_groups<float><<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.g);
+    launch_kernel(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, pl.g);
     return check_launch();
 }
 

@@ -187,7 +187,7 @@ static ks_status launch_tile(const float* in, const float* k, float* out, int64_
     }
     const int tiles = static_cast<int>((L + TileGeom<R>::T - 1) / TileGeom<R>::T);
     const int64_t blocks = B * H * tiles;
-    conv_tile_f32<R, S, FUSED><<<static_cast<unsigned>(blocks), kTileThreads, smem, st>>>(
+    launch_kernel(conv_tile_f32<R, S, FUSED>, static_cast<unsigned>(blocks), kTileThreads, smem, st, 
         in, k, out, static_cast<int>(H), static_cast<int>(L), static_cast<int>(K),
         static_cast<int>(off), reverse, tiles);
     return check_launch();
@@ -212,9 +212,9 @@ static ks_status launch_direct(const T* in, const T* k, T* out, int64_t B, int64
     const int64_t want = (total + 255) / 256;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>(want, int64_t(num_sms()) * 32));
     if (mode == KS_MULADD_FUSED)
-        conv_direct<T, true><<<blocks, 256, 0, st>>>(in, k, out, H, L, K, off, reverse, total);
+        launch_kernel(conv_direct<T, true>, blocks, 256, 0, st, in, k, out, H, L, K, off, reverse, total);
     else
-        conv_direct<T, false><<<blocks, 256, 0, st>>>(in, k, out, H, L, K, off, reverse, total);
+        launch_kernel(conv_direct<T, false>, blocks, 256, 0, st, in, k, out, H, L, K, off, reverse, total);
     return check_launch();
 }
 

@@ -164,7 +164,7 @@ ks_status ks_rank_tree_sum_f32(const float* gather, float* out, int64_t n, int w
     if (world < 1 || world > 64) return KS_ERR_SHARD;
     if (n < 0) return KS_ERR_DIM_H;
     if (n == 0) return KS_OK;
-    rank_tree_sum<<<static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+    launch_kernel(rank_tree_sum, static_cast<unsigned>((n + 255) / 256), 256, 0, static_cast<cudaStream_t>(stream), 
         gather, out, n, world);
     return check_launch();
 }

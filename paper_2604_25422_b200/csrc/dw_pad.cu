@@ -211,7 +211,7 @@ ks_status launch(const CUtensorMap& gm, const CUtensorMap& xm, float* part, int6
     auto kern = dw_pad<NJG, FUSED>;
     const int smem = dwpad_smem(g, NS);
     prepare_kernel(reinterpret_cast<const void*>(kern), kNT + 32, smem);
-    kern<<<static_cast<unsigned>(int64_t(G) * H * g.NJT), kNT + 32, smem, st>>>(
+    launch_kernel(kern, static_cast<unsigned>(int64_t(G) * H * g.NJT), kNT + 32, smem, st, 
         gm, xm, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L), static_cast<int>(K), G, g, NS);
     return check_launch();
 }

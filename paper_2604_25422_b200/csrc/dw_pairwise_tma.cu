@@ -271,7 +271,7 @@ ks_status launch(int s, const CUtensorMap& gm, const CUtensorMap& xm, const CUte
     case SV: {                                                                                                \
         auto kern = dw_pairwise_tma<NJ, SV>;                                                                  \
         prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                \
-        kern<<<blocks, kThreads, smem, st>>>(gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),      \
+        launch_kernel(kern, blocks, kThreads, smem, st, gm, xm, xt, part, static_cast<int>(B), static_cast<int>(H),      \
                                              static_cast<int>(L), static_cast<int>(K), p, G, NJT, g, NS);     \
         break;                                                                                                \
     }
@@ -346,7 +346,7 @@ ks_status dw_pairwise_tma_f32(const float* gy, const float* x, float* dk, int64_
     }
     if (rc != KS_OK) return rc;
     const int64_t HK = H * K;
-    dw_sum_groups_tree<<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, dk, HK, pl.G);
+    launch_kernel(dw_sum_groups_tree, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, pl.G);
     return check_launch();
 }
 

@@ -252,7 +252,7 @@ ks_status launch(int s, int s2, const Maps& mp, const float* k, float* part, int
     if (s == SV && s2 == S2V) {                                                                                \
         auto kern = dw_tma<JR, TB, NJ, SV, FUSED, BWD, S2V>;                                                   \
         prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                 \
-        kern<<<blocks, kThreads, smem, st>>>(mp.gm, mp.xm, mp.xt, mp.dxm, k, part, static_cast<int>(B),        \
+        launch_kernel(kern, blocks, kThreads, smem, st, mp.gm, mp.xm, mp.xt, mp.dxm, k, part, static_cast<int>(B),        \
                                              static_cast<int>(H), static_cast<int>(L), static_cast<int>(K), p, \
                                              G, NJT, g, NS);                                                   \
         return check_launch();                                                                                 \

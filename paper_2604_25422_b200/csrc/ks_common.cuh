@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "ks_dwconv1d.h"
 
 namespace ks {
@@ -66,8 +68,23 @@ int prepare_kernel(const void* func, int threads, int smem);
 // Records a CUDA error for ks_last_error_string and maps it to a status.
 ks_status cuda_status(cudaError_t e);
 // Called after every kernel launch of the library: maps a launch error to a
-// status and counts the launch (ks_launch_count).
+// status.
 ks_status check_launch();
+
+// Every kernel launch of the library goes through launch_kernel(): it records the
+// launch (kernel, grid, block, dynamic shared memory) when the calling thread
+// is planning (ks_dwconv1d_plan: the dispatch runs, nothing launches) and
+// counts it otherwise (ks_launch_count).  Returns whether to launch.
+bool note_launch(const void* fn, dim3 grid, dim3 block, size_t smem);
+
+template <typename... KArgs, typename... Args>
+inline void launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args&&... args) {
+    if (note_launch(reinterpret_cast<const void*>(kern), grid, block, smem))
+        kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+}
+// True while the calling thread is planning: no device work may be issued
+// (kernels are recorded by launch_kernel(); copies must be skipped by the caller).
+bool planning();
 void set_last_error(const char* what);
 
 // Tuning options (options.cu; ks_set_option).  Order = the table in options.cu.

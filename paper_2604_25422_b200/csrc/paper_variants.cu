@@ -210,12 +210,12 @@ ks_status run(int variant, int path, const float* a, const float* b, float* out,
         switch (variant) {
             case 0: {
                 const dim3 grid((Li + kNaiveThreads - 1) / kNaiveThreads, Hi, Bi);
-                naive_stencil<FUSED><<<grid, kNaiveThreads, 0, st>>>(a, b, out, Hi, Li, Ki, off, rev);
+                launch_kernel(naive_stencil<FUSED>, grid, kNaiveThreads, 0, st, a, b, out, Hi, Li, Ki, off, rev);
                 break;
             }
             case 1: {
                 const dim3 grid((Li + kTTile - 1) / kTTile, (Hi + kHTile - 1) / kHTile, Bi);
-                coalesced_stencil<FUSED><<<grid, kCoalThreads, 0, st>>>(a, b, out, Hi, Li, Ki, off, rev);
+                launch_kernel(coalesced_stencil<FUSED>, grid, kCoalThreads, 0, st, a, b, out, Hi, Li, Ki, off, rev);
                 break;
             }
             case 2: {
@@ -223,7 +223,7 @@ ks_status run(int variant, int path, const float* a, const float* b, float* out,
                 const size_t smem = sizeof(float) * (kTpb + 2 * Ki - 1);
                 cudaFuncSetAttribute(shared_stencil<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(std::min<size_t>(smem, 227 * 1024)));
-                shared_stencil<FUSED><<<static_cast<unsigned>(B * H * tiles), kTpb, smem, st>>>(a, b, out, Hi, Li,
+                launch_kernel(shared_stencil<FUSED>, static_cast<unsigned>(B * H * tiles), kTpb, smem, st, a, b, out, Hi, Li,
                                                                                                Ki, off, rev, tiles);
                 break;
             }
@@ -231,7 +231,7 @@ ks_status run(int variant, int path, const float* a, const float* b, float* out,
                 const size_t smem = sizeof(float) * (L + K);
                 cudaFuncSetAttribute(warp_stencil<FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      static_cast<int>(std::min<size_t>(smem, 227 * 1024)));
-                warp_stencil<FUSED><<<dim3(Bi, Hi), 32, smem, st>>>(a, b, out, Hi, Li, Ki, off, rev);
+                launch_kernel(warp_stencil<FUSED>, dim3(Bi, Hi), 32, smem, st, a, b, out, Hi, Li, Ki, off, rev);
                 break;
             }
         }
@@ -240,7 +240,7 @@ ks_status run(int variant, int path, const float* a, const float* b, float* out,
     // dW: a = gy, b = x
     if (variant == 0) {
         const dim3 grid((Ki + kNaiveThreads - 1) / kNaiveThreads, Hi);
-        naive_dw<FUSED><<<grid, kNaiveThreads, 0, st>>>(a, b, out, Bi, Hi, Li, Ki);
+        launch_kernel(naive_dw<FUSED>, grid, kNaiveThreads, 0, st, a, b, out, Bi, Hi, Li, Ki);
         return check_launch();
     }
     const int64_t n = B * L;
@@ -248,17 +248,17 @@ ks_status run(int variant, int path, const float* a, const float* b, float* out,
     float* part = static_cast<float*>(ws);
     const dim3 grid(kChunks, Hi);
     if (variant == 1) {
-        twostage_dw<false, FUSED><<<grid, 256, 0, st>>>(a, b, part, Bi, Hi, Li, Ki, span);
+        launch_kernel(twostage_dw<false, FUSED>, grid, 256, 0, st, a, b, part, Bi, Hi, Li, Ki, span);
     } else {
         const size_t smem = sizeof(float) * 2 * span;
         cudaFuncSetAttribute(twostage_dw<true, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              static_cast<int>(std::min<size_t>(smem, 227 * 1024)));
-        twostage_dw<true, FUSED><<<grid, 256, smem, st>>>(a, b, part, Bi, Hi, Li, Ki, span);
+        launch_kernel(twostage_dw<true, FUSED>, grid, 256, smem, st, a, b, part, Bi, Hi, Li, Ki, span);
     }
     ks_status s = check_launch();
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
-    sum_chunks<<<static_cast<unsigned>((HK + 255) / 256), 256, 0, st>>>(part, out, HK);
+    launch_kernel(sum_chunks, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, out, HK);
     return check_launch();
 }
 

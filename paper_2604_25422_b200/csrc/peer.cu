@@ -247,7 +247,7 @@ ks_status ks_dwconv1d_dw_f32_peer(const float* gy, const float* x, float* dk, in
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
     const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((HK + 255) / 256, int64_t(num_sms()) * 4));
-    peer_combine<<<blocks, 256, 0, st>>>(p->ptrs, dk, world, rank, G, H, K, epoch, p->failed_dev);
+    launch_kernel(peer_combine, blocks, 256, 0, st, p->ptrs, dk, world, rank, G, H, K, epoch, p->failed_dev);
     return check_launch();
 }
 

@@ -336,7 +336,7 @@ ks_status stencil_rows_f32(const float* in, const float* k, float* out, int64_t 
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), threads, static_cast<int>(smem));
     const int64_t grid = std::min<int64_t>(nchunks, int64_t(num_sms()) * per_sm);
     *handled = true;
-    kern<<<static_cast<unsigned>(grid), threads, smem, st>>>(im, k, out, nrows, static_cast<int>(H),
+    launch_kernel(kern, static_cast<unsigned>(grid), threads, smem, st, im, k, out, nrows, static_cast<int>(H),
                                                              static_cast<int>(L), static_cast<int>(K),
                                                              static_cast<int>(off), reverse,
                                                              static_cast<int>(nchunks), g);
@@ -378,7 +378,7 @@ ks_status dw_rows_stage1(const float* gy, const float* x, float* part, int64_t B
     }
     prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);
     *handled = true;
-    kern<<<blocks, threads, smem, st>>>(gm, xm, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L),
+    launch_kernel(kern, blocks, threads, smem, st, gm, xm, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L),
                                         static_cast<int>(K), G, njt, NJG, TP, BOXG, BOXX);
     return check_launch();
 }

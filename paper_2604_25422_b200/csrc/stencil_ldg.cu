@@ -89,8 +89,8 @@ ks_status launch_k(bool fused, const float* in, const float4* kp, float* out, in
     const int tpr = static_cast<int>((L + 2047) / 2048);
     const unsigned grid = static_cast<unsigned>(rows * tpr);
     const int h = static_cast<int>(H), l = static_cast<int>(L);
-    if (fused) stencil_ldg<KT, true, REV><<<grid, 256, 0, st>>>(in, kp, out, tpr, h, l);
-    else stencil_ldg<KT, false, REV><<<grid, 256, 0, st>>>(in, kp, out, tpr, h, l);
+    if (fused) launch_kernel(stencil_ldg<KT, true, REV>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+    else launch_kernel(stencil_ldg<KT, false, REV>, grid, 256, 0, st, in, kp, out, tpr, h, l);
     return check_launch();
 }
 
@@ -132,7 +132,7 @@ ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * 16, st));
     if (rc != KS_OK) return rc;
     *handled = true;
-    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st>>>(k, kp, H, K, 16,
+    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st, k, kp, H, K, 16,
                                                                                                    reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {

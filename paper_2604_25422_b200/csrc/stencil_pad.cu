@@ -261,7 +261,7 @@ ks_status launch(const CUtensorMap& im, const float* kp, float* out, int64_t B, 
     const int tiles_per_row = static_cast<int>((L + T - 1) / T);
     const int ntiles = static_cast<int>(B * H / g.RPT * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
-    kern<<<grid, threads, smem, st>>>(im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
+    launch_kernel(kern, grid, threads, smem, st, im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
                                       g, NS);
     return check_launch();
 }
@@ -332,7 +332,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     float* kp = nullptr;
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
     if (rc != KS_OK) return rc;
-    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
+    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st, 
         k, kp, H, K, g.Kp, reverse, zlead);
     rc = check_launch();
     if (rc == KS_OK) {

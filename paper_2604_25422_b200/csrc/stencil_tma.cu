@@ -196,7 +196,7 @@ ks_status launch(const CUtensorMap& im, const CUtensorMap& om, const float* kp, 
     const int tiles_per_row = static_cast<int>((L + g.T - 1) / g.T);
     const int ntiles = static_cast<int>(B * H * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
-    kern<<<grid, NT, smem, st>>>(im, om, kp, out, static_cast<int>(H), static_cast<int>(L), static_cast<int>(K),
+    launch_kernel(kern, grid, NT, smem, st, im, om, kp, out, static_cast<int>(H), static_cast<int>(L), static_cast<int>(K),
                                  tiles_per_row, ntiles, g, NS);
     return check_launch();
 }
@@ -313,7 +313,7 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     float* kp = nullptr;
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
     if (rc != KS_OK) return rc;
-    prep_taps<<<static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st>>>(
+    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st, 
         k, kp, H, K, g.Kp, reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {

@@ -1,16 +1,20 @@
 #!/usr/bin/env python3
 """The paper's kernel ablation (Table II) re-run on B200.
 
-usage: python tools/ablation.py [--shape B H L K] [--reps N] [--out profiles/r01_ablation]
+usage: python tools/ablation.py [--shape B H L K] [--reps N] [--mode separate|fused] [--out profiles/r02_ablation]
 
 Times forward / dX / dW of the four paper designs (naive, coalesced, shared,
 warp; csrc/paper_variants.cu, the reference's launch geometries) and of this
-library's kernels (variant b200: stencil_tma + dw_tma) on the paper's training
-shape (B,H,L,K) = (16384,128,48,48) by default, with CUDA events after warm-up.
-Writes <out>.csv in the reference's timing-log schema (variant,path,runtime_ms,
-run_id; src/timing_log.cpp:44-97) -- the naive/coalesced/shared/warp rows can be
-fed to the reference's own `kernelscope analyze` with a B200 device spec -- and
-<out>.md with the table and per-path effective bandwidth.
+library's kernels (variant b200) on the paper's training shape (B,H,L,K) =
+(16384,128,48,48) by default, with CUDA events after warm-up.  Writes, in the
+reference's timing-log schema (variant,path,runtime_ms,run_id;
+src/timing_log.cpp:44-97), which the reference's own analysis pipeline reads
+(oracle/_ref/ks_b200_report, with a B200 device spec):
+  <out>_paper.csv    the paper's designs that launch all three paths here;
+  <out>_library.csv  the paper's naive design (the baseline) and this library,
+                     logged under the warp-tiled id -- the design family it
+                     extends; the reference's VariantId has no fifth value;
+and <out>.md with the table and per-path effective bandwidth.
 """
 import argparse
 import os
@@ -41,9 +45,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shape", type=int, nargs=4, default=[16384, 128, 48, 48])
     ap.add_argument("--reps", type=int, default=10)
-    ap.add_argument("--out", default="profiles/r01_ablation")
+    ap.add_argument("--out", default="profiles/r02_ablation")
+    ap.add_argument("--mode", choices=["separate", "fused"], default="separate")
     a = ap.parse_args()
     B, H, L, K = a.shape
+    mode = ks.FUSED if a.mode == "fused" else ks.SEPARATE
     x, k, gy = ks.make_inputs(1, B, H, L, K)
     y = torch.empty_like(x)
     dk = torch.empty((H, K), dtype=torch.float32, device="cuda")
@@ -54,14 +60,14 @@ def main():
         res = {}
         for path in ("fwd", "dx", "dw"):
             if name == "b200":
-                fn = {"fwd": lambda: ks.forward(x, k, ks.FUSED, out=y),
-                      "dx": lambda: ks.backward_input(gy, k, ks.FUSED, out=y),
-                      "dw": lambda: ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, ks.FUSED, out=dk,
+                fn = {"fwd": lambda: ks.forward(x, k, mode, out=y),
+                      "dx": lambda: ks.backward_input(gy, k, mode, out=y),
+                      "dw": lambda: ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, mode, out=dk,
                                                        workspace=ws)}[path]
             else:
-                fn = {"fwd": lambda: ks.variant(name, "fwd", x, k, out=y),
-                      "dx": lambda: ks.variant(name, "dx", gy, k, out=y),
-                      "dw": lambda: ks.variant(name, "dw", gy, x, K, out=dk)}[path]
+                fn = {"fwd": lambda: ks.variant(name, "fwd", x, k, mode=mode, out=y),
+                      "dx": lambda: ks.variant(name, "dx", gy, k, mode=mode, out=y),
+                      "dw": lambda: ks.variant(name, "dw", gy, x, K, mode=mode, out=dk)}[path]
             try:
                 ts = time_it(fn, a.reps)
             except ks.KsError as err:
@@ -70,18 +76,29 @@ def main():
                 continue
             res[path] = sorted(ts)[len(ts) // 2]
             ref_path = {"fwd": "fwd", "dx": "bwd_in", "dw": "bwd_k"}[path]
-            for i, t in enumerate(ts):
-                rows.append(f"{'b200_tma' if name == 'b200' else name},{ref_path},{t:.6f},{i}")
+            rows.append((name, [f"{ref_path},{t:.6f},{i}" for i, t in enumerate(ts)]))
         total = sum(res.values()) if all(v is not None for v in res.values()) else None
         table.append((name, res, total))
     os.makedirs(os.path.dirname(a.out) or ".", exist_ok=True)
-    with open(a.out + ".csv", "w") as f:
-        f.write(f"# B200 ablation, shape (B,H,L,K)=({B},{H},{L},{K}), fp32 Fused, median of {a.reps}\n")
+    complete = {name for name, _, total in table if total is not None}
+    head = f"shape (B,H,L,K)=({B},{H},{L},{K}), fp32 {a.mode}, {a.reps} CUDA-event timings per path on one B200"
+    with open(a.out + "_paper.csv", "w") as f:
+        f.write(f"# the paper's kernel designs as sm_100a kernels (csrc/paper_variants.cu), {head}; "
+                f"designs that cannot launch every path at this shape are left out\n")
         f.write("variant,path,runtime_ms,run_id\n")
-        f.write("\n".join(rows) + "\n")
+        for name, rs in rows:
+            if name != "b200" and name in complete:
+                f.write("".join(f"{name},{r}\n" for r in rs))
+    with open(a.out + "_library.csv", "w") as f:
+        f.write(f"# naive = the paper's naive design; warp = THIS LIBRARY's kernels (the warp-tiled design "
+                f"family it extends; the reference's VariantId has no fifth value), {head}\n")
+        f.write("variant,path,runtime_ms,run_id\n")
+        for name, rs in rows:
+            if name in ("naive", "b200"):
+                f.write("".join(f"{'warp' if name == 'b200' else name},{r}\n" for r in rs))
     naive_total = table[0][2]
     with open(a.out + ".md", "w") as f:
-        f.write(f"# Paper ablation on one B200 — (B,H,L,K) = ({B},{H},{L},{K}), fp32, Fused\n\n")
+        f.write(f"# Paper ablation on one B200 — (B,H,L,K) = ({B},{H},{L},{K}), fp32, {a.mode}\n\n")
         f.write("Median of %d CUDA-event timings after 3 warm-ups (ms); GB/s = (8·B·H·L + 4·H·K) / time.\n\n" % a.reps)
         f.write("| variant | fwd ms | dX ms | dW ms | conv total ms | speedup vs naive | fwd GB/s | dX GB/s | dW GB/s |\n")
         f.write("|---|---|---|---|---|---|---|---|---|\n")
