@@ -543,21 +543,31 @@ def run_ours(args, cfg_name, cfg):
         if ks.lib().ks_probe_fp32_tflops(ctypes.byref(c)) == 0:
             fp32 = c.value
     if fp32:
+        # the FP32 roof in useful FLOPs per path: FMA pipe at 2 FLOP per
+        # instruction.  Forward / dX in Separate mode need two instructions per
+        # tap (FMUL + FADD, the reference's two roundings), so their roof is
+        # half; HIERARCHICAL dW accumulates with FMA in either mode.
+        sep = mode == ks.SEPARATE
+        roof = {"fwd": fp32 / 2 if sep else fp32, "dX": fp32 / 2 if sep else fp32, "dW": fp32}
         fl = path_flops(B, H, L, K)
         ufl = useful_flops(B, H, L, K)
         ach = ufl / (split_mean[dom] * 1e-3) / 1e12
-        roofline = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(fp32, 2), "unit": "TFLOP/s",
-                    "frac": round(ach / fp32, 4), "traffic": dom_traffic, "kernel": names[dom],
-                    "peak_kind": "measured in-process (ks_probe_fp32_tflops: FFMA loop on all SMs)",
+        roofline = {"bound": "fp32", "achieved": round(ach, 2), "peak": round(roof[names[dom]], 2),
+                    "unit": "TFLOP/s", "frac": round(ach / roof[names[dom]], 4), "traffic": dom_traffic,
+                    "kernel": names[dom],
+                    "peak_kind": "measured in-process (ks_probe_fp32_tflops: FFMA loop on all SMs)"
+                                 + (", halved for a Separate-mode stencil (FMUL + FADD per tap)"
+                                    if sep and names[dom] != "dW" else ""),
+                    "fp32_fma_peak": round(fp32, 2),
                     "algorithmic_flops_per_launch": ufl, "paper_flops_per_launch": fl,
-                    "frac_paper_flops": round(fl / (split_mean[dom] * 1e-3) / 1e12 / fp32, 4),
+                    "frac_paper_flops": round(fl / (split_mean[dom] * 1e-3) / 1e12 / roof[names[dom]], 4),
                     "note": "compute-bound (K/4 FLOP/B > ridge); achieved = useful FLOPs (2 x taps that touch "
                             "the row, SURVEY 8(d)) / mean CUDA-event duration of the path; the paper's "
                             "2*B*H*L*K also counts taps on the zero padding (frac_paper_flops); HBM GB/s "
                             "per path in `paths`"}
         for n in names:
-            paths[n]["frac_fp32_measured"] = round(paths[n]["TFLOP_s_useful"] / fp32, 4)
-            paths[n]["frac_fp32_paper_flops"] = round(paths[n]["TFLOP_s_paper"] / fp32, 4)
+            paths[n]["frac_fp32_roof"] = round(paths[n]["TFLOP_s_useful"] / roof[n], 4)
+            paths[n]["frac_fp32_paper_flops"] = round(paths[n]["TFLOP_s_paper"] / roof[n], 4)
     # our kernels launched inside the two timed loops (counted by the library
     # at capture / launch time: ks_launch_count)
     gpu_launches = args.steps * (sum(launches[f] for f in split_fns) +

@@ -107,7 +107,9 @@ ks_status ks_dwconv1d_dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_
  * otherwise ws_bytes must be >= ks_dwconv1d_dw_workspace_bytes(...).
  * `chunk` is only read for KS_DW_CHUNKED (chunk >= B*L degenerates to
  * SEQUENTIAL, src/conv_core.cpp:172-174); `mode` is ignored by PAIRWISE, whose
- * leaves are plain products (src/conv_core.cpp:88-95). */
+ * leaves are plain products (src/conv_core.cpp:88-95), and by HIERARCHICAL,
+ * whose order is this library's own and which always accumulates with fused
+ * multiply-add (the same dk in both modes). */
 ks_status ks_dwconv1d_dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t H,
                              int64_t L, int64_t K, int scheme, int64_t chunk, int mode,
                              void* ws, size_t ws_bytes, void* stream);
@@ -164,7 +166,10 @@ ks_status ks_get_option(const char* name, int64_t* value);
 typedef struct ks_launch_rec {
     char kernel[256]; /* demangled kernel signature */
     uint32_t grid[3], block[3];
-    uint64_t smem_bytes; /* dynamic shared memory */
+    uint64_t smem_bytes;  /* dynamic shared memory */
+    int32_t regs;         /* registers per thread (cudaFuncGetAttributes) */
+    int32_t static_smem;  /* static shared memory per CTA (cudaFuncGetAttributes) */
+    int32_t ctas_per_sm;  /* resident CTAs per SM at this block / smem (occupancy API) */
 } ks_launch_rec;
 ks_status ks_dwconv1d_plan(int path, int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                            int mode, ks_launch_rec* recs, int cap, int* n);

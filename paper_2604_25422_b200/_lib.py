@@ -93,7 +93,7 @@ _SIGS = {
 class LaunchRec(C.Structure):
     """ks_launch_rec (include/ks_dwconv1d.h)."""
     _fields_ = [("kernel", C.c_char * 256), ("grid", C.c_uint32 * 3), ("block", C.c_uint32 * 3),
-                ("smem_bytes", C.c_uint64)]
+                ("smem_bytes", C.c_uint64), ("regs", C.c_int32), ("static_smem", C.c_int32), ("ctas_per_sm", C.c_int32)]
 
 
 _lib = None

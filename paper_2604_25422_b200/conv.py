@@ -488,4 +488,6 @@ def plan(path: str, B: int, H: int, L: int, K: int, scheme: int = HIERARCHICAL, 
                                      C.byref(n))
     _raise_dims(st, f"plan {path}")
     return [{"kernel": r.kernel.decode(), "grid": tuple(r.grid), "block": tuple(r.block),
-             "smem": int(r.smem_bytes)} for r in recs[:min(n.value, cap)]]
+             "smem": int(r.smem_bytes), "regs": int(r.regs), "static_smem": int(r.static_smem),
+             "ctas_per_sm": int(r.ctas_per_sm)}
+            for r in recs[:min(n.value, cap)]]

@@ -44,6 +44,15 @@
 #ifndef KS_EVICT_FIRST
 #define KS_EVICT_FIRST 0  // 1: TMA loads / stores carry an L2 evict_first policy
 #endif
+#ifndef KS_DW_NS_SHORT
+#define KS_DW_NS_SHORT 4  // dW / fused backward stages, K <= 8
+#endif
+#ifndef KS_DW_NS_LONG
+#define KS_DW_NS_LONG 3   // dW / fused backward stages, 8 < K <= 16
+#endif
+#ifndef KS_FUSED_NS_SHORT
+#define KS_FUSED_NS_SHORT KS_DW_NS_SHORT  // fused backward stages, K <= 8
+#endif
 
 namespace ks {
 namespace bwds {
@@ -83,7 +92,9 @@ struct Geo {
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
     static constexpr int TapBytes = BASE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
     static constexpr int Stage = GYRegion + (HAS_DW ? kXRegion : 0) + TapBytes;
-    static constexpr int NS = BASE >= kFWD ? KS_ST_NS : KT <= 8 ? 4 : 3;  // dW as dw_tma: 4 stages when FMAs are light
+    static constexpr int NS = BASE >= kFWD ? KS_ST_NS
+                              : KT <= 8 ? (BASE == kFUSED ? KS_FUSED_NS_SHORT : KS_DW_NS_SHORT)
+                                        : KS_DW_NS_LONG;  // dW as dw_tma: 4 stages when FMAs are light
     static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : 3;
     static constexpr uint32_t TX =
         static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 64 : 0));
@@ -176,14 +187,14 @@ __device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob
 #pragma unroll
         for (int tt = 0; tt < 8; ++tt)
 #pragma unroll
-            for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
+            for (int jj = 0; jj < KT; ++jj) acc[jj] = muladd<true>(acc[jj], gv[tt], xv[Gm::S + tt + jj]);
     }
 }
 
 template <int KT, bool FUSED, int MODE>
 __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap* x_map, const CUtensorMap* out_map,
                                     const float* __restrict__ k, float* __restrict__ part, unsigned char* smem,
-                                    uint64_t* full, float (*red)[KT], const Args a) {
+                                    uint64_t* full, const Args a) {
     using Gm = Geo<KT, MODE>;
     constexpr int NS = Gm::NS;
     const int tid = threadIdx.x;
@@ -290,6 +301,11 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     if (Gm::HAS_OBUF && tid == 0) bulk_wait_all();
 
     if constexpr (Gm::HAS_DW) {
+        // the 8 warp partials go to stage memory (every loaded stage has been
+        // consumed by now): no static shared array, which would round the
+        // CTA's static shared memory up to 1 KiB and cost the dW kernel its
+        // third CTA per SM
+        float (*red)[KT] = reinterpret_cast<float (*)[KT]>(stages);
         // fixed xor-shuffle tree per warp, then the 8 warps in ascending order (as dw_tma)
 #pragma unroll
         for (int jj = 0; jj < KT; ++jj) {
@@ -300,7 +316,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         }
         if (lane == 0) {
 #pragma unroll
-            for (int jj = 0; jj < KT; ++jj) red[warp][jj] = acc[jj];
+            for (int jj = 0; jj < KT; ++jj) red[warp][jj] = acc[jj];  // (stage memory: every item is consumed)
         }
         __syncthreads();
         if (tid < KT) {
@@ -323,7 +339,6 @@ bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + (Gm::HAS_OBUF ? 2 * kOutBytes : 0) + Gm::NS * Gm::Stage);
-    __shared__ float red[Gm::HAS_DW ? kThreads / 32 : 1][KT];
 
     Args a;
     a.H = H;
@@ -354,7 +369,7 @@ bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
         fence_mbar_init();
     }
     __syncthreads();
-    run<KT, FUSED, MODE>(&in_map, &x_map, &out_map, k, part, smem, full, red, a);
+    run<KT, FUSED, MODE>(&in_map, &x_map, &out_map, k, part, smem, full, a);
 }
 
 }  // namespace bwds

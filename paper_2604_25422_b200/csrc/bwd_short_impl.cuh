@@ -29,8 +29,11 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
 template <int KT, int MODE>
 ks_status launch_m(bool fused, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k,
                    float* part, int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st) {
-    return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st)
-                 : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
+    // dW only: HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
+    if constexpr ((MODE & 7) == kDW) return launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
+    else
+        return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st)
+                     : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
 }
 
 template <int MODE>

@@ -131,6 +131,10 @@ int prepare_kernel(const void* func, int threads, int smem) {
     if (!lim) {
         limits.push_back({func, dev, 0});
         lim = &limits.back();
+        // ask for the largest shared-memory carveout: the driver otherwise may
+        // pick a smaller one and hold a kernel below the CTAs/SM its shared
+        // memory allows (bwd_short dW at config 3: 2 CTAs/SM where 3 fit)
+        cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     }
     if (smem > lim->smem) {
         cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -421,6 +425,7 @@ ks_status ks_dwconv1d_plan(int path, int64_t B, int64_t H, int64_t L, int64_t K,
     KS_TRY(check_mode(mode));
     if (path == 2) KS_TRY(check_dw(scheme, chunk));
     KS_TRY(check_device());
+    KS_TRY(cuda_status(cudaFree(nullptr)));  // a current context: tensor-map encoding needs one
     // placeholder operands: 1 KiB aligned, never dereferenced (nothing launches)
     auto fake = [](int i) { return reinterpret_cast<float*>(uintptr_t(0x7f0000000000ull) + (uintptr_t(i) << 36)); };
     float *a = fake(0), *b = fake(1), *c = fake(2), *d = fake(3), *e = fake(4);
@@ -457,6 +462,16 @@ ks_status ks_dwconv1d_plan(int path, int64_t B, int64_t H, int64_t L, int64_t K,
         r.grid[0] = recs_v[i].grid.x, r.grid[1] = recs_v[i].grid.y, r.grid[2] = recs_v[i].grid.z;
         r.block[0] = recs_v[i].block.x, r.block[1] = recs_v[i].block.y, r.block[2] = recs_v[i].block.z;
         r.smem_bytes = recs_v[i].smem;
+        cudaFuncAttributes fa{};
+        if (cudaFuncGetAttributes(&fa, recs_v[i].fn) == cudaSuccess) {
+            r.regs = fa.numRegs;
+            r.static_smem = static_cast<int32_t>(fa.sharedSizeBytes);
+        }
+        int occ = 0;
+        const int threads = static_cast<int>(r.block[0] * r.block[1] * r.block[2]);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, recs_v[i].fn, threads, recs_v[i].smem) == cudaSuccess)
+            r.ctas_per_sm = occ;
+        cudaGetLastError();
     }
     return KS_OK;
 }

@@ -7,7 +7,12 @@
 //  * HIERARCHICAL (fast path): in-register FMA partials over t for an 8-tap
 //    register block, a fixed warp-shuffle tree, a fixed shared-memory pass over
 //    warps, per-CTA partials [G,H,K] in global scratch, then a fixed-order
-//    cross-block pass.  Deterministic, no atomics; parity by tolerance.
+//    cross-block pass.  Deterministic, no atomics; parity by tolerance.  Its
+//    association order is this library's own, so the reference's MulAddMode
+//    does not define its bits: it always accumulates with fused multiply-add
+//    (one rounding per term -- closer to the exact sum than two, and half
+//    the instructions of Separate, which at K = 16 is the difference between
+//    an HBM-bound and an issue-bound kernel).  dk is the same in both modes.
 //  * PAIRWISE: the reference's midpoint tree over the flat index
 //    (src/conv_core.cpp:113-118), evaluated bit-exactly: the top 8 tree levels
 //    in shared memory, each depth-8 subtree by one thread.
@@ -132,7 +137,7 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
                     for (int tt = 0; tt < kTB; ++tt)
 #pragma unroll
                         for (int jj = 0; jj < kJR; ++jj)
-                            acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+                            acc[jj] = muladd<true>(acc[jj], gv[tt], xv[S + tt + jj]);
                 }
             }
             __syncthreads();
@@ -550,8 +555,7 @@ ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B
     if (!handled && L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
     if (!handled && !tma_disabled()) s = dw_tma_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
     if (!handled)
-        s = mode == KS_MULADD_FUSED ? launch_hier<true>(gy, x, part, B, H, L, K, pl, st)
-                                    : launch_hier<false>(gy, x, part, B, H, L, K, pl, st);
+        s = launch_hier<true>(gy, x, part, B, H, L, K, pl, st);
     *G = pl.g;
     return s;
 }

@@ -169,13 +169,13 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 #pragma unroll
                         for (int tt = 0; tt < kTW; ++tt) {
                             const int jj = m - tt;
-                            if (jj >= 0 && jj < kJR) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[m]);
+                            if (jj >= 0 && jj < kJR) acc[jj] = muladd<true>(acc[jj], gv[tt], xv[m]);
                         }
                 } else {
 #pragma unroll
                     for (int tt = 0; tt < kTW; ++tt)
 #pragma unroll
-                        for (int jj = 0; jj < kJR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[tt + jj]);
+                        for (int jj = 0; jj < kJR; ++jj) acc[jj] = muladd<true>(acc[jj], gv[tt], xv[tt + jj]);
                 }
             };
             window(0);
@@ -278,17 +278,13 @@ ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B,
     CUtensorMap gm, xm;
     if (!encode_padded_view(&gm, gy, B * H, L, H, g.gy_rows, 1, 1)) return KS_OK;
     if (!encode_padded_view(&xm, x, B * H, L, H, g.NBX, 1, 1)) return KS_OK;
-    const bool fused = mode == KS_MULADD_FUSED;
+    (void)mode;  // HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
     *handled = true;
     switch (njg) {
-        case 4: return fused ? launch<4, true>(gm, xm, part, B, H, L, K, G, g, NS, st)
-                             : launch<4, false>(gm, xm, part, B, H, L, K, G, g, NS, st);
-        case 8: return fused ? launch<8, true>(gm, xm, part, B, H, L, K, G, g, NS, st)
-                             : launch<8, false>(gm, xm, part, B, H, L, K, G, g, NS, st);
-        case 16: return fused ? launch<16, true>(gm, xm, part, B, H, L, K, G, g, NS, st)
-                              : launch<16, false>(gm, xm, part, B, H, L, K, G, g, NS, st);
-        default: return fused ? launch<32, true>(gm, xm, part, B, H, L, K, G, g, NS, st)
-                              : launch<32, false>(gm, xm, part, B, H, L, K, G, g, NS, st);
+        case 4: return launch<4, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
+        case 8: return launch<8, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
+        case 16: return launch<16, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
+        default: return launch<32, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
     }
 }
 

@@ -169,7 +169,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 #pragma unroll
                 for (int tt = 0; tt < TB; ++tt)
 #pragma unroll
-                    for (int jj = 0; jj < JR; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+                    for (int jj = 0; jj < JR; ++jj) acc[jj] = muladd<true>(acc[jj], gv[tt], xv[S + tt + jj]);
                 if constexpr (BWD) {
                     // dx[t0+tl+r] = sum_j gy[t0+tl+r+j-q] * k[K-1-j], j ascending from +0
                     float v2[4 * NV2];
@@ -321,14 +321,15 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
     if (bwd)
         return j16 ? launch_m<16, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st)
                    : launch_m<8, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
-    if (j16) return launch_m<16, 8, 1, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+    // dW only: HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
+    if (j16) return launch<16, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     if (JR == 8)
-        return nj == 1 ? launch_m<8, 8, 1, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st)
-                       : launch_m<8, 8, 2, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        return nj == 1 ? launch<8, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st)
+                       : launch<8, 8, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     switch (nj) {
-        case 2: return launch_m<16, 16, 2, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
-        case 4: return launch_m<16, 16, 4, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
-        default: return launch_m<16, 16, 8, false>(s, 0, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        case 2: return launch<16, 16, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        case 4: return launch<16, 16, 4, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        default: return launch<16, 16, 8, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     }
 }
 

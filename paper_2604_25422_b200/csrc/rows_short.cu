@@ -264,7 +264,7 @@ dw_rows(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUte
 #pragma unroll
                 for (int tt = 0; tt < 8; ++tt)
 #pragma unroll
-                    for (int jj = 0; jj < kJB; ++jj) acc[jj] = muladd<FUSED>(acc[jj], gv[tt], xv[S + tt + jj]);
+                    for (int jj = 0; jj < kJB; ++jj) acc[jj] = muladd<true>(acc[jj], gv[tt], xv[S + tt + jj]);
             }
         }
         __syncthreads();  // stage consumed
@@ -365,15 +365,15 @@ ks_status dw_rows_stage1(const float* gy, const float* x, float* part, int64_t B
     const cuuint32_t boxg[3] = {static_cast<cuuint32_t>(BOXG), 1, 32};
     const cuuint32_t boxx[3] = {static_cast<cuuint32_t>(BOXX), 1, 32};
     if (!encode_rows(&gm, gy, 3, dims, boxg) || !encode_rows(&xm, x, 3, dims, boxx)) return KS_OK;
-    const bool fused = mode == KS_MULADD_FUSED;
+    (void)mode;  // HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
     const unsigned blocks = static_cast<unsigned>(int64_t(G) * H * njt);
     const int threads = 32 * NJG * TP;
     const int p4 = static_cast<int>((4 - (K / 2) % 4) % 4);  // (j0 - p) mod 4 with j0 % 8 == 0
-    auto kern = fused ? dw_rows<0, true> : dw_rows<0, false>;
+    auto kern = dw_rows<0, true>;
     switch (p4) {
-        case 1: kern = fused ? dw_rows<1, true> : dw_rows<1, false>; break;
-        case 2: kern = fused ? dw_rows<2, true> : dw_rows<2, false>; break;
-        case 3: kern = fused ? dw_rows<3, true> : dw_rows<3, false>; break;
+        case 1: kern = dw_rows<1, true>; break;
+        case 2: kern = dw_rows<2, true>; break;
+        case 3: kern = dw_rows<3, true>; break;
         default: break;
     }
     prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);

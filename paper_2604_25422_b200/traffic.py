@@ -17,16 +17,51 @@ model) extends to B200:
   (TMA boxes overlap by 32*HH floats per side per tile);
 * ``plan(path, B, H, L, K)`` -- which kernel family runs, its tile and grid
   (mirrors the host dispatch in csrc/: conv_fwd.cu, stencil_ldg.cu,
-  stencil_tma.cu, bwd_short.cuh, stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu).
+  stencil_tma.cu, bwd_short.cuh, stencil_pad.cu, rows_short.cu, conv_dw.cu, dw_*.cu);
+* ``launch_geometry(path, B, H, L, K)`` -- every launch of the call (kernel
+  family, grid, block, dynamic shared memory), the counterpart of the
+  reference's ``launch_geometry`` (exec_model.hpp:14-60);
+* ``shared_mem_footprint(path, B, H, L, K)`` -- dynamic shared memory of the
+  call's main kernel, the counterpart of the reference's
+  ``shared_mem_footprint`` (exec_model.hpp:62-80);
+* ``resource_check(...)`` -- resident CTAs per SM from shared memory, threads
+  and registers (the reference's ``resource_check``, exec_model.cpp:136-166).
 
-``tests/test_traffic.py`` checks memory_traffic against the ncu DRAM bytes
-committed in profiles/ncu_summary.json.
+Pinned, on the CPU, by ``tests/test_traffic.py`` against what the hardware
+and the library report: memory_traffic against ncu's DRAM bytes for configs
+2, 3, 4, 5a and 5b (profiles/ncu_summary.json), launch_geometry /
+shared_mem_footprint / plan against the library's own dispatch run without
+launching (ks_dwconv1d_plan, profiles/r02_plans.json, every config and the
+multi-GPU shards).
 """
 from __future__ import annotations
 
 import math
 
 SMS = 148
+SMEM_PER_SM = 233472     # bytes (228 KiB) of shared memory per SM at the largest carveout
+SMEM_RESERVED = 1024     # per resident CTA (the runtime's)
+REGS_PER_SM = 65536
+THREADS_PER_SM = 2048
+MAX_CTAS_PER_SM = 32
+
+
+def resource_check(threads: int, smem: int, regs: int | None = None, static_smem: int = 0) -> int:
+    """Resident CTAs per SM (the reference's resource_check,
+    src/exec_model.cpp:136-166, with sm_100's limits): the smallest of the
+    shared-memory (dynamic + static + the runtime's 1 KiB per CTA), thread,
+    register and CTA-slot limits.  Registers are allocated per warp in units
+    of 256."""
+    per_cta = smem + static_smem + SMEM_RESERVED
+    lim = [MAX_CTAS_PER_SM, THREADS_PER_SM // threads, SMEM_PER_SM // per_cta]
+    if regs:
+        per_warp = -(-regs * 32 // 256) * 256
+        lim.append(REGS_PER_SM // (per_warp * -(-threads // 32)))
+    return max(0, min(lim))
+
+
+def _cdiv(a: int, b: int) -> int:
+    return -(-a // b)
 
 
 def logical_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
@@ -66,7 +101,7 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
         nj *= 2
     njt = math.ceil(K / (nj * 8))
     G = max(1, min(math.ceil(8192 / (H * njt)), B))
-    if L < 2048 and L % 4 == 0:
+    if L < 2048 and L % 4 == 0 and L + 8 * min(8, groups8) + 16 <= 252:  # dw_rows: a whole row in one TMA box
         return "dw_rows", G
     if L % 32 == 0 and K <= 16:
         return "dw_short", G  # bwd_short.cuh MODE dW: dw_tma's decomposition, K-specialised
@@ -97,35 +132,228 @@ def plan(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical"
     return {"kernel": name, "row_groups": G, "partials_bytes": 4 * G * H * K}
 
 
-def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> int:
-    """Modeled DRAM bytes per launch of the B200 kernels."""
+def memory_traffic_rw(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> tuple:
+    """Modeled DRAM (read, write) bytes of one entry-point call, all its
+    launches: the compulsory tensor bytes, the taps staging (prep_taps reads k
+    and writes kp, which the kernel reads back) and dW's per-CTA partials
+    (written by stage 1, read back by the fixed-order pass).  Halo re-reads
+    hit L2 (each halo is a neighbouring tile's body) and are not DRAM bytes."""
+    T = 4 * B * H * L
+    kb = 4 * H * K
     if path == "bwd":
         p = plan(path, B, H, L, K)
         if p["kernel"] == "split":
-            return memory_traffic("dx", B, H, L, K) + memory_traffic("dw", B, H, L, K)
-        # one pass: read gy and x, write dx, read k; partials out and back
-        return 12 * B * H * L + 4 * H * K + 2 * p["partials_bytes"]
-    base = logical_traffic(path, B, H, L, K)
+            a, b = memory_traffic_rw("dx", B, H, L, K), memory_traffic_rw("dw", B, H, L, K)
+            return a[0] + b[0], a[1] + b[1]
+        # one pass: read gy, x and k, write dx; partials out and back; dk out
+        return 2 * T + kb + p["partials_bytes"], T + p["partials_bytes"] + kb
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
+        staged = p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short", "stencil_ldg")
         kp = 4 * H * (16 if p["kernel"] in ("stencil_short", "stencil_ldg") else math.ceil(K / 32) * 32)
-        # prep_taps writes kp, the kernel reads it back
-        return base + (2 * kp if p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short", "stencil_ldg") else 0)
+        return T + kb + (kp if staged else 0), T + (kp if staged else 0)
     if p["kernel"] == "dw_pairwise_tma":
-        return base
-    return base + 2 * p["partials_bytes"]  # partials written by stage 1, read by stage 2
+        return 2 * T, kb
+    return 2 * T + p["partials_bytes"], p["partials_bytes"] + kb
+
+
+def memory_traffic(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> int:
+    """Modeled DRAM bytes (read + write) of one entry-point call."""
+    return sum(memory_traffic_rw(path, B, H, L, K, scheme))
+
+
+def halo_bytes(path: str, B: int, H: int, L: int, K: int) -> int:
+    """Bytes a forward / dX call re-reads beyond the tensor: every tile's
+    window overhangs its outputs by the halo (the neighbouring tiles' bodies).
+    They are L2 hits while the neighbour's data is resident, DRAM re-reads
+    otherwise -- a persistent grid visits a row's tiles far apart, so at long K
+    (stencil_pad: a 4096-output tile carries a Kp-wide window overhang) a few
+    percent of the tensor is read twice from DRAM (ncu: 3.9% at config 5c)."""
+    if path == "bwd":
+        p = plan(path, B, H, L, K)
+        if p["kernel"] == "split":
+            return halo_bytes("dx", B, H, L, K)
+        return B * H * _cdiv(L, 2048) * 2 * 128  # the gy box's halo piece on each side of a 2048-wide item
+    if path not in ("fwd", "dx"):
+        return 0
+    p = plan(path, B, H, L, K)
+    off = K // 2 if path == "fwd" else K - 1 - K // 2
+    if p["kernel"] == "stencil_ldg":  # window quads past each 2048-output tile (the rest hits L1)
+        return B * H * _cdiv(L, 2048) * 2 * 4 * math.ceil((max(off, K - 1 - off) + 3) / 4) * 4
+    if p["kernel"] == "stencil_pad":
+        lead = (32 - off % 32) % 32
+        Kp = _cdiv(K + lead - (lead & 3), 32) * 32
+        return B * H * _cdiv(L, 4096) * (Kp + 32) * 4
+    if not p["tiles"]:
+        return 0
+    HH = 1 if p["kernel"] == "stencil_short" else max(1, math.ceil(max(off, K - 1 - off) / 32))
+    return p["tiles"] * 2 * 32 * HH * 4
 
 
 def l2_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
-    """Modeled L2->SM bytes of the stencil kernels: each tile re-reads its
-    halo (32*HH floats per side) from L2."""
-    p = plan(path, B, H, L, K)
-    if path not in ("fwd", "dx") or not p["tiles"]:
-        return memory_traffic(path, B, H, L, K)
-    off = K // 2 if path == "fwd" else K - 1 - K // 2
-    if p["kernel"] == "stencil_ldg":  # window quads past each 2048-output tile (the rest hits L1)
-        halo = p["tiles"] * 2 * 4 * math.ceil((max(off, K - 1 - off) + 3) / 4) * 4
-        return memory_traffic(path, B, H, L, K) + halo
-    HH = 1 if p["kernel"] == "stencil_short" else max(1, math.ceil(max(off, K - 1 - off) / 32))
-    halo = p["tiles"] * 2 * 32 * HH * 4
-    return memory_traffic(path, B, H, L, K) + halo
+    """Modeled L2->SM bytes: the DRAM model plus every halo re-read."""
+    return memory_traffic(path, B, H, L, K) + halo_bytes(path, B, H, L, K)
+
+
+# ---------------------------------------------------------------------------
+# launch geometry (grid, block, dynamic shared memory) per kernel family
+
+def _launch(kernel, grid, block, smem):
+    return {"kernel": kernel, "grid": int(grid), "block": int(block), "smem": int(smem)}
+
+
+def _prep_taps(H: int, Kp: int):
+    return _launch("prep_taps", min(_cdiv(H * Kp, 256), 4096), 256, 0)
+
+
+def _bwd_short(mode: str, B, H, L, K, G, occ):
+    """bwd_short.cuh Geo<KT, MODE>: 144-byte pieces, a 66-piece x window."""
+    gyp = 64 if mode == "dw" else 66
+    gy_region = _cdiv(gyp * 144, 128) * 128
+    x_region = _cdiv(66 * 144, 128) * 128
+    has_dw, has_st = mode in ("dw", "fused"), mode in ("fused", "fwd", "dx")
+    stage = gy_region + (x_region if has_dw else 0) + (128 if mode in ("fwd", "dx") else 0)
+    ns = 4 if mode in ("fwd", "dx") else (4 if K <= 8 else 3)
+    smem = (2 * 8192 if has_st else 0) + ns * stage + 64 + 1024
+    grid = G * H if has_dw else min(B * H, SMS * occ(256, smem))
+    return _launch("bwd_short", grid, 256, smem)
+
+
+def _stencil_pad(B, H, L, K, off, occ):
+    """stencil_pad.cu PadGeom: 128 FMA threads x 32 outputs, 36-float rows."""
+    nt, kr = 128, 32
+    lead = (32 - off % 32) % 32
+    S = lead & 3
+    Kp = _cdiv(K + lead - S, 32) * 32
+    rpt = 1
+    while rpt < 4 and nt * kr // (2 * rpt) >= L and H % (2 * rpt) == 0:
+        rpt *= 2
+    T = nt // rpt * kr
+    nr = T // 32 + Kp // 32 + (1 if S >= 2 else 0)
+    nbox, nb = (1, nr) if nr <= 256 else (2, ((nr + 1) // 2 + 7) // 8 * 8)
+    stage = _cdiv(rpt * nbox * nb * 36 * 4 + rpt * Kp * 4, 1024) * 1024
+    ns = 1 if K >= 1024 else 3
+    while ns > 1 and ns * stage + 1152 > 110 * 1024:
+        ns -= 1
+    smem = ns * stage + 128 + 1024
+    threads = nt + (32 if K < 1024 else 0)
+    tiles = B * H // rpt * _cdiv(L, T)
+    return [_prep_taps(H, Kp), _launch("stencil_pad", min(tiles, SMS * occ(threads, smem)), threads, smem)]
+
+
+def _dw_pad(B, H, L, K, G):
+    """dw_pad.cu DwPadGeom: 256 FMA threads + a producer warp, 32 taps per thread."""
+    p = K // 2
+    base = p % 32 - 32 if p % 32 else 0
+    kk = K - base
+    njg = 4
+    while njg < 32 and njg * 32 < kk:
+        njg *= 2
+    nts = 256 // njg
+    jt = njg * 32
+    njt = _cdiv(kk, jt)
+    tt = min(max(min(max(64 * nts, 4096), L), 32 * nts), 8192)
+    gy_rows = tt // 32
+    gy_alloc = _cdiv(gy_rows, 8) * 8
+    xr = (tt + jt) // 32
+    nbx, NBX = (1, xr) if xr <= 256 else (2, _cdiv(_cdiv(xr, 2), 8) * 8)
+    stage = _cdiv((gy_alloc + nbx * NBX) * 144, 1024) * 1024
+    ns = 3
+    while ns > 2 and max(ns * stage, 256 * 33 * 4) + 1152 > 110 * 1024:
+        ns -= 1
+    smem = max(ns * stage, 256 * 33 * 4) + 128 + 1024
+    return _launch("dw_pad", G * H * njt, 288, smem)
+
+
+def _dw_tma(B, H, L, K, G):
+    """dw_tma.cu: 2048-wide work items, JR x TB register blocks, nj tap groups."""
+    jr = 8 if K <= 8 else 16
+    nj = 1 if (jr == 8 or K <= 16) else 2
+    while nj < 8 and nj * jr < K:
+        nj *= 2
+    njt = _cdiv(K, nj * jr)
+    gy_bytes = _cdiv(64 * 32 * 4, 1024) * 1024
+    xt = _cdiv(nj * jr + 40, 32)
+    stage = _cdiv(gy_bytes + (64 + xt) * 128, 1024) * 1024
+    ns = max(2, min(3 if K > 8 else 4, 72 * 1024 // stage))
+    return _launch("dw_tma", G * H * njt, 256, ns * stage + 64 + 1024)
+
+
+def _stride4(n: int) -> int:
+    return _cdiv(n - 4, 32) * 32 + 4
+
+
+def _stencil_rows(B, H, L, K, off, occ):
+    sh = (4 - off % 4) % 4
+    box = _stride4(L + K - 1 + sh)
+    ks_ = _stride4(_cdiv(K, 8) * 8 + 4)
+    segs = _cdiv(L, 16)
+    nrc = min(max(32, (256 // segs) // 32 * 32), 256)
+    stage = nrc * box
+    ns = 3
+    smem_of = lambda n: (n * stage + H * ks_) * 4 + 64 + 128  # noqa: E731
+    while ns > 2 and smem_of(ns) > 110 * 1024:
+        ns -= 1
+    smem = smem_of(ns)
+    threads = min(256, nrc * segs)
+    return _launch("stencil_rows", min(_cdiv(B * H, nrc), SMS * occ(threads, smem)), threads, smem)
+
+
+def _dw_rows(B, H, L, K, G):
+    g8 = _cdiv(K, 8)
+    njg = min(8, g8)
+    tp = max(1, 8 // njg)
+    njt = _cdiv(g8, njg)
+    boxg, boxx = _stride4(L + 4), _stride4(L + njg * 8 + 16)
+    return _launch("dw_rows", G * H * njt, 32 * njg * tp, 2 * 32 * (boxg + boxx) * 4 + 64 + 128)
+
+
+def launch_geometry(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical", occ=None) -> list:
+    """Every launch of one entry-point call, in order: kernel family, grid,
+    block, dynamic shared memory.  ``occ(threads, smem)`` gives resident CTAs
+    per SM for the persistent kernels (default: resource_check without the
+    register limit; ks_dwconv1d_plan reports the occupancy API's value)."""
+    occ = occ or (lambda t, sm: resource_check(t, sm))
+    pl = plan(path, B, H, L, K, scheme)
+    if path == "bwd":
+        if pl["kernel"] == "split":
+            return launch_geometry("dx", B, H, L, K, occ=occ) + launch_geometry("dw", B, H, L, K, occ=occ)
+        return [_bwd_short("fused", B, H, L, K, pl["row_groups"], occ),
+                _launch("dw_sum_groups", _cdiv(H * K, 256), 256, 0)]
+    if path in ("fwd", "dx"):
+        off = K // 2 if path == "fwd" else K - 1 - K // 2
+        kind = pl["kernel"]
+        if kind == "stencil_ldg":
+            return [_prep_taps(H, 16), _launch("stencil_ldg", B * H * _cdiv(L, 2048), 256, 0)]
+        if kind == "stencil_short":
+            return [_prep_taps(H, 16), _bwd_short(path, B, H, L, K, 1, occ)]
+        if kind == "stencil_pad":
+            return _stencil_pad(B, H, L, K, off, occ)
+        if kind == "stencil_rows":
+            return [_stencil_rows(B, H, L, K, off, occ)]
+        raise NotImplementedError(kind)
+    kind, G = pl["kernel"], pl.get("row_groups")
+    tail = [_launch("dw_sum_groups", _cdiv(H * K, 256), 256, 0)]
+    if kind == "dw_short":
+        return [_bwd_short("dw", B, H, L, K, G, occ)] + tail
+    if kind == "dw_pad":
+        return [_dw_pad(B, H, L, K, G)] + tail
+    if kind == "dw_rows":
+        return [_dw_rows(B, H, L, K, G)] + tail
+    if kind == "dw_tma":
+        return [_dw_tma(B, H, L, K, G)] + tail
+    raise NotImplementedError(kind)
+
+
+def shared_mem_footprint(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical") -> int:
+    """Dynamic shared memory (bytes per CTA) of the call's main kernel."""
+    return max(g["smem"] for g in launch_geometry(path, B, H, L, K, scheme))
+
+
+def kernel_family(signature: str) -> str:
+    """'void ks::(anonymous namespace)::stencil_pad<0, false, false>(...)' (the
+    library's demangled names) or 'void <unnamed>::stencil_pad<0, 0, 0>(...)'
+    (ncu's) -> 'stencil_pad', the family names launch_geometry uses."""
+    s = signature.replace("(anonymous namespace)::", "").replace("<unnamed>::", "")
+    s = s.split("(")[0].replace("void ", "").strip()
+    return s.split("<")[0].split("::")[-1]

@@ -553,3 +553,45 @@ def test_nccl_combine_single_rank():
         assert same(host(dk), ref)
     finally:
         comm.close()
+
+
+@pytest.mark.parametrize("name", ["config1", "config2", "config3", "config4", "config5a", "config5b", "config5c",
+                                  "config4_g8", "config5b_g8", "paper"])
+def test_plan_is_current_and_matches_what_launches(name):
+    """ks_dwconv1d_plan (the dispatch run without launching) reproduces the
+    committed plans the CPU traffic-model tests pin (profiles/r02_plans.json),
+    and on a batch-reduced copy of the shape the real call launches exactly
+    as many kernels as its plan lists (ks_launch_count)."""
+    with open(os.path.join(ROOT, "profiles", "r02_plans.json")) as f:
+        want = json.load(f)[name]
+    B, H, L, K = want["shape"]
+    for path in ("fwd", "dx", "dw", "bwd"):
+        got = ks.plan(path, B, H, L, K)
+        strip = lambda rs: [(r["kernel"], r["grid"], r["block"], r["smem"]) for r in rs]  # noqa: E731
+        assert strip(got) == [(r["kernel"], tuple(r["grid"]), tuple(r["block"]), r["smem"]) for r in want[path]], path
+    b = max(1, min(B, (1 << 26) // (H * L)))
+    x, k, gy = ks.make_inputs(5, b, H, L, K)
+    torch.cuda.synchronize()
+    for path, fn in (("fwd", lambda: ks.forward(x, k, SEPARATE)), ("dx", lambda: ks.backward_input(gy, k, SEPARATE)),
+                     ("dw", lambda: ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, SEPARATE)),
+                     ("bwd", lambda: ks.backward(gy, x, k, SEPARATE))):
+        c0 = ks.launch_count()
+        fn()
+        torch.cuda.synchronize()
+        assert ks.launch_count() - c0 == len(ks.plan(path, b, H, L, K)), path
+
+
+def test_hierarchical_dw_is_mode_independent():
+    """HIERARCHICAL dW accumulates with FMA in either MulAddMode (its order is
+    the library's own): dk bit-identical across modes, through dW and through
+    the fused backward, while dx keeps each mode's reference bits."""
+    for B, H, L, K in ((4, 8, 4096, 7), (3, 4, 2048, 16), (2, 4, 2048, 200), (16, 8, 48, 48), (3, 2, 1000, 9)):
+        x, k, gy = ks.make_inputs(8, B, H, L, K)
+        a = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, SEPARATE))
+        b = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+        assert same(a, b), (B, H, L, K)
+        dxs, dks = ks.backward(gy, x, k, SEPARATE)
+        dxf, dkf = ks.backward(gy, x, k, FUSED)
+        assert same(host(dks), a) and same(host(dkf), a)
+        assert same(host(dxs), host(ks.backward_input(gy, k, SEPARATE)))
+        assert same(host(dxf), host(ks.backward_input(gy, k, FUSED)))

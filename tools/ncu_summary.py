@@ -3,6 +3,15 @@
 
 usage: python tools/ncu_summary.py ROUND [--launches gpurun_out/launches.csv]
                                    [--full name=gpurun_out/prof_x.ncu-rep ...]
+       python tools/ncu_summary.py ROUND --config NAME --shape B H L K --run-shape LIST.csv
+
+The --shape form reads the launch list of `tools/run_shape.py B H L K --reps 1
+--bwd` (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,
+dram__bytes_write.sum,launch__grid_size,launch__block_size,
+launch__shared_mem_per_block_dynamic): three fill launches, then the fwd, dX,
+dW and backward calls, segmented by the B200 traffic model's launch counts
+(traffic.launch_geometry), into profiles/<ROUND>_launches_<NAME>.csv and
+ncu_summary.json[NAME][fwd|dX|dW|bwd] = {dram_read, dram_write, ...}.
 
 Writes
   profiles/<ROUND>_launches.csv      per-launch device time + DRAM bytes (the
@@ -108,17 +117,69 @@ def launches(csv_path, rnd):
     return per
 
 
+def run_shape_list(csv_path, rnd, config, shape):
+    sys.path.insert(0, ROOT)
+    from paper_2604_25422_b200 import traffic
+    with open(csv_path) as f:
+        text = f.read()
+    rows = list(csv.reader(io.StringIO(text[text.index('"ID"'):])))
+    hdr = rows[0]
+    ix = {k: hdr.index(k) for k in hdr}
+    per = {}
+    for r in rows[1:]:
+        if len(r) < len(hdr):
+            continue
+        key = (int(r[ix["ID"]]), r[ix["Kernel Name"]])
+        per.setdefault(key, {})[r[ix["Metric Name"]]] = num(r[ix["Metric Value"]])
+    launches_ = sorted(per.items())
+    B, H, L, K = shape
+    segs, i = {}, 3  # make_inputs: three fill launches first
+    for path, name in (("fwd", "fwd"), ("dx", "dX"), ("dw", "dW"), ("bwd", "bwd")):
+        n = len(traffic.launch_geometry(path, B, H, L, K))
+        segs[name] = launches_[i:i + n]
+        i += n
+    out = os.path.join(PROF, f"{rnd}_launches_{config}.csv")
+    with open(out, "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["path", "id", "kernel", "grid", "block", "smem", "time_us", "dram_read_bytes", "dram_write_bytes"])
+        for name, ls in segs.items():
+            for (i_, kname), m in ls:
+                w.writerow([name, i_, kname[:110], int(m.get("launch__grid_size") or 0),
+                            int(m.get("launch__block_size") or 0), int(m.get("launch__shared_mem_per_block_dynamic") or 0),
+                            round((m.get("gpu__time_duration.sum") or 0) / 1e3, 2),
+                            int(m.get("dram__bytes_read.sum") or 0), int(m.get("dram__bytes_write.sum") or 0)])
+    print("wrote", out)
+    res = {}
+    for name, ls in segs.items():
+        rd = sum(m.get("dram__bytes_read.sum") or 0 for _, m in ls)
+        wr = sum(m.get("dram__bytes_write.sum") or 0 for _, m in ls)
+        main_ = max(ls, key=lambda kv: kv[1].get("gpu__time_duration.sum") or 0)
+        res[name] = {"dram_bytes": int(rd + wr), "dram_read": int(rd), "dram_write": int(wr),
+                     "launches": len(ls), "kernel": traffic.kernel_family(main_[0][1]),
+                     "ncu_time_us": round(sum((m.get("gpu__time_duration.sum") or 0) for _, m in ls) / 1e3, 2),
+                     "round": rnd, "shape": list(shape)}
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("round")
     ap.add_argument("--launches")
     ap.add_argument("--full", nargs="*", default=[])
     ap.add_argument("--config", default="config3")
+    ap.add_argument("--shape", type=int, nargs=4)
+    ap.add_argument("--run-shape")
     a = ap.parse_args()
     os.makedirs(PROF, exist_ok=True)
     summ_path = os.path.join(PROF, "ncu_summary.json")
     summ = json.load(open(summ_path)) if os.path.exists(summ_path) else {}
     cfg = summ.setdefault(a.config, {})
+    if a.run_shape:
+        cfg.update(run_shape_list(a.run_shape, a.round, a.config, a.shape))
+        with open(summ_path, "w") as f:
+            json.dump(summ, f, indent=1, sort_keys=True)
+        print("wrote", summ_path)
+        return 0
     if a.launches:
         per = launches(a.launches, a.round)
         # per-path DRAM bytes from the last complete fwd/dX/dW triple

@@ -30,10 +30,16 @@ def timed(fn, reps):
 
 ap = argparse.ArgumentParser()
 ap.add_argument("shape", type=int, nargs=4)
+ap.add_argument("--mode", choices=["separate", "fused"], default="separate")
+ap.add_argument("--opt", action="append", default=[], help="tuning option name=value (ks_set_option)")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--paths", default="fwd,dx,dw,bwd")
 a = ap.parse_args()
 B, H, L, K = a.shape
+MODE = ks.FUSED if a.mode == "fused" else ks.SEPARATE
+for kv in a.opt:
+    name, val = kv.split("=")
+    ks.set_option(name, int(val))
 x, k, gy = ks.make_inputs(1, B, H, L, K)
 y = torch.empty_like(x)
 dx = torch.empty_like(x)
@@ -42,16 +48,16 @@ n = B * H * L
 out = {}
 paths = a.paths.split(",")
 if "fwd" in paths:
-    ms = timed(lambda: ks.forward(x, k, ks.FUSED, out=y), a.reps)
+    ms = timed(lambda: ks.forward(x, k, MODE, out=y), a.reps)
     out["fwd"] = (ms, 8 * n / ms / 1e6)
 if "dx" in paths:
-    ms = timed(lambda: ks.backward_input(gy, k, ks.FUSED, out=dx), a.reps)
+    ms = timed(lambda: ks.backward_input(gy, k, MODE, out=dx), a.reps)
     out["dx"] = (ms, 8 * n / ms / 1e6)
 if "dw" in paths:
-    ms = timed(lambda: ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, ks.FUSED), a.reps)
+    ms = timed(lambda: ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, MODE), a.reps)
     out["dw"] = (ms, 8 * n / ms / 1e6)
 if "bwd" in paths:
-    ms = timed(lambda: ks.backward(gy, x, k, ks.FUSED, out=(dx, dk)), a.reps)
+    ms = timed(lambda: ks.backward(gy, x, k, MODE, out=(dx, dk)), a.reps)
     out["bwd"] = (ms, 12 * n / ms / 1e6)
 ms = timed(lambda: y.copy_(x), a.reps)
 out["copy"] = (ms, 8 * n / ms / 1e6)
