@@ -31,7 +31,10 @@
  *    no floating-point atomics anywhere.
  *  - Rounding: y and dX accumulate taps in ascending j from +0, exactly like
  *    the reference loops (src/conv_core.cpp:37-40, 66-69), so they are
- *    bit-identical to the reference in both MulAddModes.  dW schemes
+ *    bit-identical to the reference in both MulAddModes for finite inputs.
+ *    (The kernels multiply the zero padding where the reference skips a tap:
+ *    with an Inf or NaN among the inputs, outputs within K of it may be NaN
+ *    where the reference's are not; every other output keeps its bits.)  dW schemes
  *    SEQUENTIAL / PAIRWISE / CHUNKED reproduce the reference association order
  *    bit-for-bit (src/conv_core.cpp:98-146); HIERARCHICAL is this library's
  *    fast deterministic order (parity within a stated tolerance).

@@ -18,6 +18,18 @@
 // nearest never yields -0 from a +0 start) -- the same argument that makes the
 // zero-filled halo exact -- so results stay bit-identical to the reference.
 //
+// Zero-halo tap blocks are skipped per LANE: a tap block whose x positions
+// all fall outside the row only multiplies TMA's zero fill.  A warp covers
+// 1024 consecutive outputs, so where K is comparable to L (config 2, K = L)
+// its lanes' valid block ranges are shifted by one block per lane; skipping
+// per warp still computes the union (~31 blocks of ~96 per lane: 25% of the
+// FFMAs on zeros), skipping per lane computes each lane's own range (the
+// loop diverges by at most a block).  Warps whose lanes agree (every warp
+// away from the row ends) keep warp-uniform bounds, so their taps stay
+// provably uniform.  Taps are staged at the window's 36-float pitch per
+// 32-tap block, so lanes reading different blocks are 144 B apart
+// (conflict-free), as the window reads are.
+//
 // Tiles: RPT consecutive channels of one batch entry x (TPR*32)-output pieces
 // of their rows; NT = 128 threads (one warp per SM sub-partition), thread
 // (r, lt) owns outputs [t0 + 32 lt, +32) of channel h0 + r.  NS-stage TMA ring
@@ -58,7 +70,19 @@ constexpr bool use_antidiag() {
 
 namespace ks {
 
-__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
+// kp[h] = `lead` zeros, then k[h, j] (forward) or k[h, K-1-j] (dX), zero
+// padded -- laid out at a 36-float pitch per 32-tap block (the window's
+// padded layout), Kpp = Kp / 32 * 36 floats per row.
+__global__ void prep_taps_pad36(const float* __restrict__ k, float* __restrict__ kp, int64_t H, int64_t K,
+                                int64_t Kpp, int reverse, int lead) {
+    const int64_t n = H * Kpp;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t h = i / Kpp, q = i - h * Kpp, blk = q / 36, c = q - blk * 36;
+        const int64_t j = blk * 32 + c - lead;
+        kp[i] = c < 32 && j >= 0 && j < K ? k[h * K + (reverse ? K - 1 - j : j)] : 0.f;
+    }
+}
 
 namespace {
 
@@ -71,10 +95,12 @@ struct PadGeom {
     int NR;            // padded 36-float rows per channel window (T/32 + Kp/32 [+1])
     int NB, nbox;      // rows per TMA box, boxes per channel window (RPT == 1 when nbox > 1)
     int Kp;            // taps (with lead zeros) padded to a multiple of 32
+    int Kpp;           // Kp / 32 * 36: staged tap row (36-float pitch per 32-tap block)
     int Ke;            // taps incl. lead zeros (the live ones)
     int base_row;      // (off + lead) / 32: window origin = t0/32 - base_row
     int off, zlead;    // stencil offset, leading zero taps (tap block jb covers j = 32 jb - zlead ...)
-    int skip;          // drop zero-halo tap blocks (KS_PAD_SKIP=0: compute them)
+    int skip;          // drop zero-halo tap blocks (option pad_skip=0: compute them)
+    int mirror;        // balance each warp's lanes: pair outputs mirrored about the row centre
     int win_floats;    // RPT * nbox * NB * 36
     int stage_bytes;   // window + RPT tap rows, 1024-aligned
 };
@@ -90,7 +116,7 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
 #pragma unroll
     for (int r = 0; r < kR; ++r) acc[r] = 0.f;
-    auto window = [&](const float* base, const int sub, const float* w16, int nj) {
+    auto window = [&](const float* base, const int sub, const float* w16, int nj) {  // w16: 16 taps
         float v[4 * NV];
 #pragma unroll
         for (int c = 0; c < NV; ++c) {
@@ -138,14 +164,16 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     const int jend = min(Kfull, jb_hi * 32);
     for (int j0 = jb_lo * 32; j0 < jend; j0 += 32) {
         const float* b0 = pw + pbase + (j0 >> 5) * 36;
-        window(b0, 0, wk + j0, kJS);
-        window(b0, 16, wk + j0 + 16, kJS);
+        const float* w0 = wk + (j0 >> 5) * 36;
+        window(b0, 0, w0, kJS);
+        window(b0, 16, w0 + 16, kJS);
     }
     if (Kfull < Ke && (Kfull >> 5) >= jb_lo && (Kfull >> 5) < jb_hi) {
         const float* b0 = pw + pbase + (Kfull >> 5) * 36;
+        const float* w0 = wk + (Kfull >> 5) * 36;
         const int rem = Ke - Kfull;
-        window(b0, 0, wk + Kfull, rem < kJS ? rem : kJS);
-        if (rem > kJS) window(b0, 16, wk + Kfull + 16, rem - kJS);
+        window(b0, 0, w0, rem < kJS ? rem : kJS);
+        if (rem > kJS) window(b0, 16, w0 + 16, rem - kJS);
     }
 }
 
@@ -164,7 +192,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     const int tid = threadIdx.x;
     const int T = g.TPR * kR;
     const int ngroups = H / g.RPT;  // channel groups per batch entry
-    const uint32_t tx_bytes = static_cast<uint32_t>(g.win_floats * 4 + g.RPT * g.Kp * 4);
+    const uint32_t tx_bytes = static_cast<uint32_t>(g.win_floats * 4 + g.RPT * g.Kpp * 4);
     auto issue = [&](int stage, int tile) {
         const int rg = tile / tiles_per_row;
         const int t0 = (tile - rg * tiles_per_row) * T;
@@ -174,8 +202,8 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         const int r0 = t0 / 32 - g.base_row;
         tma_load_pad(sb, &in_map, r0, h0, b, &full[stage]);
         if (g.nbox > 1) tma_load_pad(sb + g.NB * 144, &in_map, r0 + g.NB, h0, b, &full[stage]);
-        bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kp,
-                  static_cast<uint32_t>(g.RPT * g.Kp) * 4u, &full[stage]);
+        bulk_load(sb + g.win_floats * 4, kp + static_cast<int64_t>(h0) * g.Kpp,
+                  static_cast<uint32_t>(g.RPT * g.Kpp) * 4u, &full[stage]);
     };
 
     if (tid == 0) {
@@ -212,25 +240,46 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     // so the compiler can prove the tap addresses warp-uniform and keep the
     // taps in uniform registers
     const int rsub = use_shfl<S, PROD>() ? __shfl_sync(0xffffffffu, tid / g.TPR, 0) : tid / g.TPR;
-    const int lt = tid - rsub * g.TPR;
+    // lt: this thread's 32-output register tile within the channel row.  With
+    // `mirror` (a tile spans the whole row and K is comparable to L, where an
+    // output's valid tap count is ~ K - |t - L/2|), lane pairs take tiles
+    // mirrored about the row's centre and each warp a ring of them, so a
+    // warp's lanes have similar counts and the per-lane block bounds below
+    // leave little divergence; the rings rotate over the warps with the CTA
+    // and the tile, so the heavy centre ring does not always land on the same
+    // SM sub-partition (warp w of every CTA shares one).  Lanes stay
+    // conflict-free (lt mod 8 distinct per quarter-warp).
+    const int q = tid - rsub * g.TPR;
+    const int nwr = g.TPR / 32;
     const int win_rows = g.nbox * g.NB;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int stage = it % NS;
+        const int ring = ((q >> 5) + static_cast<int>(blockIdx.x) + it) % nwr;
+        const int lt = !g.mirror ? q
+                                 : ((q & 1) ? g.TPR / 2 + 16 * ring + ((q & 31) >> 1)
+                                            : g.TPR / 2 - 1 - 16 * ring - ((q & 31) >> 1));
         mbar_wait(&full[stage], static_cast<uint32_t>((it / NS) & 1));
         const float* sw = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const int rg = tile / tiles_per_row;
         const int t0 = (tile - rg * tiles_per_row) * T;
         const bool live = t0 + lt * kR < L;  // L % 32 == 0: a register tile is wholly in or out
-        // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
+        // this lane's outputs t in [ts, ts + 32): tap block jb reads x at
         // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
-        const int tw = t0 + (lt & ~31) * kR;
-        const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
-        const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
+        const int ts = t0 + lt * kR;
+        int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (ts + kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
+        int jb_hi = g.skip ? (L + g.off + g.zlead - ts + 31) / 32 : g.Kp / 32;
+        // warp-uniform bounds where the lanes agree (taps provably uniform),
+        // per-lane bounds near the row ends
+        const int lo0 = __shfl_sync(0xffffffffu, jb_lo, 0), hi0 = __shfl_sync(0xffffffffu, jb_hi, 0);
+        const bool agree = __all_sync(0xffffffffu, jb_lo == lo0 && jb_hi == hi0);
         float acc[kR];
-        if (live)
-            tile32<S, FUSED, use_antidiag<S, PROD>()>(sw + rsub * win_rows * 36, sw + g.win_floats + rsub * g.Kp, lt * 36, g.Ke, jb_lo, jb_hi,
-                             acc);
+        const float* pw_r = sw + rsub * win_rows * 36;
+        const float* wk_r = sw + g.win_floats + rsub * g.Kpp;
+        if (live) {
+            if (agree) tile32<S, FUSED, use_antidiag<S, PROD>()>(pw_r, wk_r, lt * 36, g.Ke, lo0, hi0, acc);
+            else tile32<S, FUSED, false>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+        }
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
         } else {
@@ -299,14 +348,17 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     const int S = lead & 3, zlead = lead - S;
     g.Ke = static_cast<int>(K) + zlead;
     g.Kp = (g.Ke + 31) / 32 * 32;
+    g.Kpp = g.Kp / 32 * 36;
     g.base_row = static_cast<int>((off + lead) / 32);
     g.off = static_cast<int>(off);
     g.zlead = zlead;
     g.skip = opt(kOptPadSkip) != 0;
+    g.mirror = 0;  // set below, once the tile width is known
     g.RPT = 1;
     while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;
     g.TPR = NT / g.RPT;
     const int T = g.TPR * kR;
+    g.mirror = g.skip && T >= L && 4 * K >= L && g.TPR % 64 == 0;
     g.NR = T / 32 + g.Kp / 32 + (S >= 2 ? 1 : 0);  // S >= 2: 13-quad windows read 4 floats further
     if (g.NR <= 256) {
         g.nbox = 1;
@@ -318,7 +370,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
         return KS_OK;
     }
     g.win_floats = g.RPT * g.nbox * g.NB * 36;
-    g.stage_bytes = (g.win_floats * 4 + g.RPT * g.Kp * 4 + 1023) / 1024 * 1024;
+    g.stage_bytes = (g.win_floats * 4 + g.RPT * g.Kpp * 4 + 1023) / 1024 * 1024;
     if (B * H / g.RPT * ((L + T - 1) / T) >= (int64_t(1) << 31)) return KS_OK;
     // stages: two in flight beyond the one being computed while the CTA count
     // per SM stays >= 2; long K (>= 1024) computes ~100x longer than it loads
@@ -330,10 +382,10 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     if (!encode_padded_view(&im, in, B * H, L, H, g.NB, g.RPT, 1)) return KS_OK;
 
     float* kp = nullptr;
-    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kp, st));
+    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kpp, st));
     if (rc != KS_OK) return rc;
-    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st, 
-        k, kp, H, K, g.Kp, reverse, zlead);
+    launch_kernel(prep_taps_pad36, static_cast<unsigned>(std::min<int64_t>((H * g.Kpp + 255) / 256, 4096)), 256, 0,
+                  st, k, kp, H, K, g.Kpp, reverse, zlead);
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;

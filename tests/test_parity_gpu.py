@@ -595,3 +595,29 @@ def test_hierarchical_dw_is_mode_independent():
         assert same(host(dks), a) and same(host(dkf), a)
         assert same(host(dxs), host(ks.backward_input(gy, k, SEPARATE)))
         assert same(host(dxf), host(ks.backward_input(gy, k, FUSED)))
+
+
+@pytest.mark.parametrize("shape", [(2, 3, 2048, 7), (2, 2, 4096, 100), (2, 2, 1024, 64), (3, 2, 48, 48),
+                                   (2, 2, 4096, 4096), (2, 3, 2048, 16)])
+def test_non_finite_inputs_contract(oracle, shape):
+    """The bitwise claims are for finite inputs (every other test).  With Inf /
+    NaN in x or k: every output the reference makes non-finite is
+    non-finite here too, and every output that differs from the reference is
+    NaN here -- the kernels multiply TMA's zero fill (and stencil_pad's leading
+    zero taps) where the reference skips the tap, so 0 * Inf = NaN can appear
+    within K of a non-finite value; they never turn a finite output into a
+    different finite one."""
+    B, H, L, K = shape
+    x, k, gy = oracle.fill_inputs(17, B, H, L, K)
+    x[0, 0, 5] = np.inf
+    x[B - 1, H - 1, L - 3] = np.nan
+    gy[0, H - 1, L // 2] = -np.inf
+    if K > 1:
+        k[0, 1] = np.inf
+    for m in (SEPARATE, FUSED):
+        for got, ref in ((host(ks.forward(dev(x), dev(k), m)), oracle.forward(x, k, m)),
+                         (host(ks.backward_input(dev(gy), dev(k), m)), oracle.backward_input(gy, k, m))):
+            assert (~np.isfinite(got))[~np.isfinite(ref)].all()
+            diff = got.view(np.uint32) != ref.view(np.uint32)
+            assert np.isnan(got[diff]).all()
+            assert diff.sum() < got.size  # the rest is bit-identical
