@@ -335,10 +335,20 @@ def run_ours(args, cfg_name, cfg):
     if world != args.gpus and world == 1 and args.gpus > 1:
         print("bench.py: --gpus N>1 must be launched under torchrun", file=sys.stderr)
         return 2
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # --transport host: the ranks' plumbing is a gloo group and the dW combine
+    # runs over the library's host communicator, so ranks may share a GPU
+    # (this is how the N > 1 path of this script is exercised on one B200;
+    # NCCL refuses two ranks on one device)
+    host_tx = args.transport == "host"
+    local_dev = local % max(1, torch.cuda.device_count()) if host_tx else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if host_tx:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    red_dev = torch.device("cpu") if host_tx else dev  # where the timing max-reductions live
     Bc, H, L, K = cfg
     conf = bench_config(cfg_name, args, world)
     B_total = conf["global_batch"]
@@ -350,10 +360,18 @@ def run_ours(args, cfg_name, cfg):
     scheme = {"hierarchical": ks.HIERARCHICAL, "pairwise": ks.PAIRWISE}[args.scheme]
 
     comm = peer = None
-    if world > 1:
+    if world > 1 and host_tx:
+        def _allgather(data: bytes):
+            t = torch.frombuffer(bytearray(data), dtype=torch.uint8)
+            out = [torch.empty_like(t) for _ in range(world)]
+            dist.all_gather(out, t)
+            return [o.numpy().tobytes() for o in out]
+        comm = ks.Comm.host(world, rank, _allgather)
+    elif world > 1:
         uid = [ks.Comm.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = ks.Comm(uid[0], world, rank)
+    if comm is not None:
         if args.combine == "peer" and scheme == ks.HIERARCHICAL:
             # NVLink peer-memory combine fused into dW (global plan: = the 1-GPU bits when shards align)
             peer = comm.peer(B, H, L, K, B_total=B_total)
@@ -466,7 +484,7 @@ def run_ours(args, cfg_name, cfg):
     split_mean = per_split.mean(axis=0)  # fwd, dX, dW, combine
     step_mean = per_step.mean(axis=0)    # fwd, bwd (or dX, dW), combine
     if world > 1:
-        t = torch.tensor([ms_total] + split_mean.tolist() + step_mean.tolist(), dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total] + split_mean.tolist() + step_mean.tolist(), dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         v = t.cpu().numpy()
         ms_total, split_mean, step_mean = float(v[0]), v[1:1 + len(split_mean)], v[1 + len(split_mean):]
@@ -621,7 +639,7 @@ def run_ours(args, cfg_name, cfg):
                 fn()
             t_host = (time.perf_counter() - t0) / e2e_steps
             if world > 1:
-                tt = torch.tensor([t_host], dtype=torch.float64, device=dev)
+                tt = torch.tensor([t_host], dtype=torch.float64, device=red_dev)
                 dist.all_reduce(tt, op=dist.ReduceOp.MAX)
                 t_host = float(tt[0])
             # the e2e roof: the step's PCIe bytes at the link's measured rates
@@ -654,8 +672,10 @@ def run_ours(args, cfg_name, cfg):
             "data": "synthetic (reference splitmix64 stream, generated on device)",
             "config": conf,
             "run": {"parallelism": f"batch-shard dp{world}" + (
-                        "" if world == 1 else " + dW combine fused over NVLink peer memory" if peer is not None
-                        else " + NCCL dW allreduce"),
+                        "" if world == 1 else " + dW combine fused over peer memory" if peer is not None
+                        else " + NCCL dW allreduce" if not host_tx else " + dW allreduce over the host communicator"),
+                    "transport": args.transport,
+                    "gpus_visible": torch.cuda.device_count(),
                     "rows_this_rank": B,
                     "l2": "inputs larger than L2 (no flush)" if flush is None
                           else "L2 flushed before every timed step (512 MB write, untimed)",
@@ -695,7 +715,10 @@ def main():
                     help="MulAddMode (the reference's default is Separate)")
     ap.add_argument("--scheme", choices=["hierarchical", "pairwise"], default="hierarchical")
     ap.add_argument("--combine", choices=["nccl", "peer"], default="nccl",
-                    help="N>1 dW combine: one ncclAllReduce, or the fused NVLink peer-memory kernel")
+                    help="N>1 dW combine: one allreduce, or the fused NVLink peer-memory kernel")
+    ap.add_argument("--transport", choices=["nccl", "host"], default="nccl",
+                    help="N>1 plumbing: NCCL (one GPU per rank), or gloo + the library's host communicator "
+                         "(ranks may share a GPU: the N>1 code path on a 1-GPU box)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--timing-log", default=None,

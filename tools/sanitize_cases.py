@@ -45,8 +45,10 @@ for (B, H, L, K) in shapes:
 # (2400,16,48,48): short-row chunks reused round the stage ring (paper shape rows)
 # (40,16,2080,16), (8,4,4160,13): K-specialised short-kernel stencils (persistent,
 # more rows than CTAs), dW and fused backward with ragged last tiles
+# (2,4,4096,4096), (3,8,1024,1024): K comparable to L -> stencil_pad's mirrored,
+# rotating lane rings with per-lane zero-halo bounds
 for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48),
-                     (40, 16, 2080, 16), (8, 4, 4160, 13)]:
+                     (40, 16, 2080, 16), (8, 4, 4160, 13), (2, 4, 4096, 4096), (3, 8, 1024, 1024)]:
     x, k, gy = o.fill_inputs(5, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
     y = ks.forward(dx_, dk_, 1)
@@ -63,4 +65,15 @@ for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150)
     truth = o.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
     err = np.abs(dk.cpu().numpy()[:1] - truth).max() / np.abs(truth).max()
     assert err <= 1e-4, err
+# unaligned bases: HIERARCHICAL dW stages the inputs into aligned scratch
+x, k, gy = o.fill_inputs(9, 3, 4, 2048, 16)
+buf = torch.empty(2 * x.size + 8, device="cuda")
+xs_ = buf[1:1 + x.size].view(x.shape)
+gs_ = buf[x.size + 5:x.size + 5 + x.size].view(x.shape)
+xs_.copy_(torch.from_numpy(x))
+gs_.copy_(torch.from_numpy(gy))
+a = ks.backward_weight(gs_, xs_, 16, ks.HIERARCHICAL, 0, 1)
+b = ks.backward_weight(torch.from_numpy(gy).cuda(), torch.from_numpy(x).cuda(), 16, ks.HIERARCHICAL, 0, 1)
+torch.cuda.synchronize()
+assert torch.equal(a.view(torch.int32), b.view(torch.int32))
 print("sanitize cases ok")
