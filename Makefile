@@ -50,7 +50,7 @@ TEST_BIN := tests/cpp/test_dropin
 tests: $(TEST_BIN) refsuite
 
 $(TEST_BIN): tests/cpp/test_dropin.cpp $(LIB) tests/cpp/doctest_shim/doctest.h oracle
-	$(CXX) -O2 -std=c++20 -Wall -Iinclude -Itests/cpp/doctest_shim -Ioracle -o $@ $< \
+	$(CXX) -O2 -std=c++20 -Wall -Iinclude -Itests/cpp/doctest_shim -Ioracle -o $@ $< -lpthread \
 	    -L$(PKG) -lks_dwconv1d -Loracle -loracle \
 	    -Wl,-rpath,'$$ORIGIN/../../$(PKG)' -Wl,-rpath,'$$ORIGIN/../../oracle'
 
@@ -61,7 +61,7 @@ ifneq ($(wildcard $(REF_ROOT)/tests/test_conv_core.cpp),)
 refsuite: oracle/_ref/ref_test_conv_core
 oracle/_ref/ref_test_conv_core: $(REF_ROOT)/tests/test_conv_core.cpp $(LIB) tests/cpp/doctest_shim/doctest.h
 	@mkdir -p oracle/_ref
-	$(CXX) -O2 -std=c++20 -Iinclude -Itests/cpp/doctest_shim -I$(REF_ROOT)/tests -o $@ $< \
+	$(CXX) -O2 -std=c++20 -Iinclude -Itests/cpp/doctest_shim -I$(REF_ROOT)/tests -o $@ $< -lpthread \
 	    -L$(PKG) -lks_dwconv1d -Wl,-rpath,'$$ORIGIN/../../$(PKG)'
 else
 refsuite:

@@ -682,7 +682,10 @@ def run_ours(args, cfg_name, cfg):
                     "cuda_graphs": bool(graphs),
                     "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)",
                     "frac_hbm_measured": round(value / world / peak, 4), "frac_hbm_8TBs": round(value / world / 8000, 4)},
-            "paths": paths, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+            "paths": paths,
+            "step_paths_ms": {n: round(float(v), 4) for n, v in zip(
+                (["fwd", "bwd"] if fused_bwd else ["fwd", "dX", "dW"]) + ["combine"], step_mean)},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
             **({"e2e_step": e2e_step} if e2e_step else {}),
             **({"e2e_note": e2e_note} if e2e_note else {}),
             "gpu_launches": gpu_launches,

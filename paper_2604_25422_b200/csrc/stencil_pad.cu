@@ -181,7 +181,10 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
 // consumer thread releases a stage as soon as it is done with it (moderate K,
 // where tiles are short); !PROD: thread 0 refills a stage after a CTA barrier
 // (long K, K >= 1024, where one stage suffices and the barrier is rare).
-template <int S, bool FUSED, bool PROD>
+// LANEB: per-lane zero-halo bounds with the mirrored, rotating lane rings
+// (g.mirror: K comparable to L); otherwise the round-1 per-warp bounds over
+// the warp's 1024 consecutive outputs, warp-uniform by construction.
+template <int S, bool FUSED, bool PROD, bool LANEB>
 __global__ void __launch_bounds__(kNT + (PROD ? 32 : 0))
 stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out,
             int H, int L, int tiles_per_row, int ntiles, PadGeom g, int NS) {
@@ -255,30 +258,32 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int stage = it % NS;
-        const int ring = ((q >> 5) + static_cast<int>(blockIdx.x) + it) % nwr;
-        const int lt = !g.mirror ? q
-                                 : ((q & 1) ? g.TPR / 2 + 16 * ring + ((q & 31) >> 1)
-                                            : g.TPR / 2 - 1 - 16 * ring - ((q & 31) >> 1));
+        const int ring = LANEB ? ((q >> 5) + static_cast<int>(blockIdx.x) + it) % nwr : 0;
+        const int lt = !LANEB ? q
+                              : ((q & 1) ? g.TPR / 2 + 16 * ring + ((q & 31) >> 1)
+                                         : g.TPR / 2 - 1 - 16 * ring - ((q & 31) >> 1));
         mbar_wait(&full[stage], static_cast<uint32_t>((it / NS) & 1));
         const float* sw = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const int rg = tile / tiles_per_row;
         const int t0 = (tile - rg * tiles_per_row) * T;
         const bool live = t0 + lt * kR < L;  // L % 32 == 0: a register tile is wholly in or out
-        // this lane's outputs t in [ts, ts + 32): tap block jb reads x at
-        // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
-        const int ts = t0 + lt * kR;
-        int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (ts + kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
-        int jb_hi = g.skip ? (L + g.off + g.zlead - ts + 31) / 32 : g.Kp / 32;
-        // warp-uniform bounds where the lanes agree (taps provably uniform),
-        // per-lane bounds near the row ends
-        const int lo0 = __shfl_sync(0xffffffffu, jb_lo, 0), hi0 = __shfl_sync(0xffffffffu, jb_hi, 0);
-        const bool agree = __all_sync(0xffffffffu, jb_lo == lo0 && jb_hi == hi0);
         float acc[kR];
         const float* pw_r = sw + rsub * win_rows * 36;
         const float* wk_r = sw + g.win_floats + rsub * g.Kpp;
-        if (live) {
-            if (agree) tile32<S, FUSED, use_antidiag<S, PROD>()>(pw_r, wk_r, lt * 36, g.Ke, lo0, hi0, acc);
-            else tile32<S, FUSED, false>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+        if constexpr (LANEB) {
+            // this lane's outputs t in [ts, ts + 32): tap block jb reads x at
+            // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
+            const int ts = t0 + lt * kR;
+            const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (ts + kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
+            const int jb_hi = g.skip ? (L + g.off + g.zlead - ts + 31) / 32 : g.Kp / 32;
+            if (live) tile32<S, FUSED, false>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+        } else {
+            // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
+            // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
+            const int tw = t0 + (lt & ~31) * kR;
+            const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
+            const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
+            if (live) tile32<S, FUSED, use_antidiag<S, PROD>()>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
         }
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
@@ -302,7 +307,7 @@ int pad_smem(const PadGeom& g, int NS) { return NS * g.stage_bytes + 128 + 1024;
 template <int S, bool FUSED, bool PROD>
 ks_status launch(const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H, int64_t L,
                  const PadGeom& g, int NS, cudaStream_t st) {
-    auto kern = stencil_pad<S, FUSED, PROD>;
+    auto kern = g.mirror ? stencil_pad<S, FUSED, PROD, true> : stencil_pad<S, FUSED, PROD, false>;
     constexpr int threads = kNT + (PROD ? 32 : 0);
     const int smem = pad_smem(g, NS);
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), threads, smem);

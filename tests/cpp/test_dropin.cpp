@@ -10,6 +10,8 @@
 
 #include <cmath>
 #include <cstring>
+#include <thread>
+#include <vector>
 
 #include "kernelscope/conv_core.hpp"
 #include "kernelscope/rng.hpp"
@@ -146,4 +148,46 @@ TEST_CASE("validate on the GPU keeps the reference's bounds") {
     CHECK(rep.fwd.max_abs > 0.0);
     CHECK(rep.bwd_in.max_abs <= 4e-6);
     CHECK(rep.dk_spread_abs > 0.0);
+}
+
+TEST_CASE("concurrent callers: the drop-in is safe for concurrent use (SPEC.md:120-121)") {
+    // 8 host threads call forward / backward_input / backward_weight at once,
+    // each on its own shape and data (every call takes its own streams and the
+    // library's scratch pool, first created under a lock); every result must
+    // equal the same call made alone.
+    constexpr int kThreads = 8;
+    std::vector<ConvShape> shapes;
+    std::vector<Case> cases;
+    for (int i = 0; i < kThreads; ++i) {
+        shapes.push_back(ConvShape(2 + i % 3, 3 + i % 2, 2048 + 32 * i, 3 + 2 * i));
+        cases.push_back(make_case(shapes.back(), 100 + static_cast<std::uint64_t>(i)));
+    }
+    struct Out {
+        Tensor3 y{1, 1, 1}, dx{1, 1, 1};
+        Kernel2 dk{1, 1}, dkh{1, 1};
+    };
+    auto run = [&](int i, Out& o) {
+        const auto& s = shapes[static_cast<std::size_t>(i)];
+        const auto& c = cases[static_cast<std::size_t>(i)];
+        const auto mode = i % 2 ? MulAddMode::Fused : MulAddMode::Separate;
+        o.y = conv::forward(c.x, c.k, s, mode);
+        o.dx = conv::backward_input(c.gy, c.k, s, mode);
+        o.dk = conv::backward_weight(c.gy, c.x, s, AccumulationScheme::chunked(512), mode);
+        o.dkh = conv::backward_weight(c.gy, c.x, s, AccumulationScheme::hierarchical(), mode);
+    };
+    std::vector<Out> alone(kThreads), together(kThreads);
+    for (int i = 0; i < kThreads; ++i) run(i, alone[static_cast<std::size_t>(i)]);
+    for (int rep = 0; rep < 3; ++rep) {
+        std::vector<std::thread> ts;
+        for (int i = 0; i < kThreads; ++i) ts.emplace_back(run, i, std::ref(together[static_cast<std::size_t>(i)]));
+        for (auto& t : ts) t.join();
+        for (int i = 0; i < kThreads; ++i) {
+            const auto& a = alone[static_cast<std::size_t>(i)];
+            const auto& b = together[static_cast<std::size_t>(i)];
+            CHECK(same_bits(a.y.data, b.y.data));
+            CHECK(same_bits(a.dx.data, b.dx.data));
+            CHECK(same_bits(a.dk.data, b.dk.data));
+            CHECK(same_bits(a.dkh.data, b.dkh.data));
+        }
+    }
 }

@@ -28,7 +28,7 @@ def test_help_runs_without_a_gpu():
 
 
 def test_committed_bench_lines_keep_the_contract():
-    lines = sorted(glob.glob(os.path.join(ROOT, "profiles", "r01_bench_config*.json")))
+    lines = sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_bench_config*.json")))
     assert lines
     for p in lines:
         with open(p) as f:
@@ -42,8 +42,29 @@ def test_committed_bench_lines_keep_the_contract():
         assert d["gpu_launches"] > 0, p
 
 
+def _line(name):
+    with open(os.path.join(ROOT, "profiles", name)) as f:
+        return json.loads(f.read().strip().splitlines()[-1])
+
+
 def test_headline_line_has_e2e_and_cpu_baseline():
-    with open(os.path.join(ROOT, "profiles", "r01_bench_config3.json")) as f:
-        d = json.loads(f.read().strip().splitlines()[-1])
+    d = _line("r02_bench_config3.json")
     assert d["e2e"]["h2d_bytes_per_step"] > 0 and d["e2e"]["d2h_bytes_per_step"] > 0
+    assert "fwd,dx,dw" in d["e2e"]["path"]  # the drop-in's three host calls are the headline e2e
+    assert d["e2e_step"]["h2d_bytes_per_step"] < d["e2e"]["h2d_bytes_per_step"]
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert "Separate" in d["cpu_baseline"]["sample"]
+
+
+def test_both_arms_share_config_and_bytes():
+    """The reference arm and this repo's arm print identical config dicts and
+    count the same compulsory bytes, so the driver's value ratio is the time
+    ratio and its same_config check holds."""
+    ours, ref = _line("r02_bench_config3.json"), _line("r02_bench_reference_config3.json")
+    assert ours["config"] == ref["config"]
+    assert ours["config"]["mode"] == "separate"  # the reference's default MulAddMode
+    B, H, L, K = (ours["config"][k] for k in "BHLK")
+    assert ours["config"]["bytes_per_step"] == bench.step_bytes(B, H, L, K) == 20 * B * H * L + 12 * H * K
+    assert abs(ours["value"] - ours["config"]["bytes_per_step"] / (ours["ms_per_step"] * 1e-3) / 1e9) < 1.0
+    assert ref["impl"] == "reference" and ref["e2e"]["h2d_bytes_per_step"] == 0
+    assert ref["side"]["mode"] == "fused"

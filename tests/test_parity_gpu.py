@@ -621,3 +621,40 @@ def test_non_finite_inputs_contract(oracle, shape):
             diff = got.view(np.uint32) != ref.view(np.uint32)
             assert np.isnan(got[diff]).all()
             assert diff.sum() < got.size  # the rest is bit-identical
+
+
+def test_concurrent_host_threads_device_calls():
+    """Host threads issuing device-pointer calls at once, each on its own
+    stream (ctypes releases the GIL around the C calls): every result equals
+    the same call made alone, bit for bit -- the reference's "safe for
+    unlimited concurrent use"."""
+    import threading
+    shapes = [(3, 4, 2048, 7), (2, 4, 4096, 16), (2, 3, 2048, 130), (4, 2, 1024, 64), (8, 4, 48, 48), (2, 2, 1000, 9)]
+    ins = [ks.make_inputs(40 + i, *s) for i, s in enumerate(shapes)]
+    torch.cuda.synchronize()
+
+    def run(i, out):
+        x, k, gy = ins[i]
+        K = shapes[i][3]
+        m = FUSED if i % 2 else SEPARATE
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            out[i] = (ks.forward(x, k, m), ks.backward_input(gy, k, m),
+                      ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m), ks.backward(gy, x, k, m))
+        s.synchronize()
+
+    alone = {}
+    for i in range(len(shapes)):
+        run(i, alone)
+    for _ in range(3):
+        together = {}
+        ts = [threading.Thread(target=run, args=(i, together)) for i in range(len(shapes))]
+        for t in ts:
+            t.start()
+        for t in ts:
+            t.join()
+        torch.cuda.synchronize()
+        for i in range(len(shapes)):
+            a, b = alone[i], together[i]
+            for u, v in zip(a[:3] + a[3], b[:3] + b[3]):
+                assert same(host(u), host(v)), i

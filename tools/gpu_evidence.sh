@@ -37,6 +37,7 @@ $T ncu --set full --clock-control none --import-source on -k regex:"stencil_pad|
 $T ncu --set full --clock-control none --import-source on -k regex:"bwd_short" -s 4 -c 4 -o $O/full_config5a python tools/run_shape.py 64 1024 16384 16 --reps 2 --bwd > $O/ncu_full5a.log 2>&1
 for r in full_config3 full_config2 full_config4 full_config5a; do
   ncu -i $O/$r.ncu-rep --page raw --csv > $O/$r.raw.csv 2>/dev/null
+  rm -f $O/$r.ncu-rep  # gpurun copies back at most 64 MiB
 done
 # sanitizers on the small cases (TMA rings, mbarriers, the mirrored stencil, unaligned staging)
 for tool in memcheck racecheck synccheck; do
