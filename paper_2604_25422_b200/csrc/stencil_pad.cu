@@ -70,6 +70,8 @@ constexpr bool use_antidiag() {
 
 namespace ks {
 
+__global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, int);
+
 // kp[h] = `lead` zeros, then k[h, j] (forward) or k[h, K-1-j] (dX), zero
 // padded -- laid out at a 36-float pitch per 32-tap block (the window's
 // padded layout), Kpp = Kp / 32 * 36 floats per row.
@@ -95,7 +97,7 @@ struct PadGeom {
     int NR;            // padded 36-float rows per channel window (T/32 + Kp/32 [+1])
     int NB, nbox;      // rows per TMA box, boxes per channel window (RPT == 1 when nbox > 1)
     int Kp;            // taps (with lead zeros) padded to a multiple of 32
-    int Kpp;           // Kp / 32 * 36: staged tap row (36-float pitch per 32-tap block)
+    int Kpp;           // staged tap row: Kp, or Kp / 32 * 36 with `mirror` (36-float pitch per 32-tap block)
     int Ke;            // taps incl. lead zeros (the live ones)
     int base_row;      // (off + lead) / 32: window origin = t0/32 - base_row
     int off, zlead;    // stencil offset, leading zero taps (tap block jb covers j = 32 jb - zlead ...)
@@ -110,7 +112,7 @@ struct PadGeom {
 // address pw + pbase (a 32-aligned logical index) and S = 0..3 the sub-quad
 // offset of its first tap.  Each 16-tap register window takes
 // ceil((S + 47) / 4) 128-bit loads (12 for S <= 1, 13 otherwise).
-template <int S, bool FUSED, bool ANTID>
+template <int S, bool FUSED, bool ANTID, int TP>  // TP: staged tap pitch per 32-tap block (32 or 36)
 __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pbase, int Ke, int jb_lo, int jb_hi,
                                        float (&acc)[kR]) {
     constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
@@ -164,13 +166,13 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     const int jend = min(Kfull, jb_hi * 32);
     for (int j0 = jb_lo * 32; j0 < jend; j0 += 32) {
         const float* b0 = pw + pbase + (j0 >> 5) * 36;
-        const float* w0 = wk + (j0 >> 5) * 36;
+        const float* w0 = TP == 32 ? wk + j0 : wk + (j0 >> 5) * TP;
         window(b0, 0, w0, kJS);
         window(b0, 16, w0 + 16, kJS);
     }
     if (Kfull < Ke && (Kfull >> 5) >= jb_lo && (Kfull >> 5) < jb_hi) {
         const float* b0 = pw + pbase + (Kfull >> 5) * 36;
-        const float* w0 = wk + (Kfull >> 5) * 36;
+        const float* w0 = TP == 32 ? wk + Kfull : wk + (Kfull >> 5) * TP;
         const int rem = Ke - Kfull;
         window(b0, 0, w0, rem < kJS ? rem : kJS);
         if (rem > kJS) window(b0, 16, w0 + 16, rem - kJS);
@@ -276,14 +278,14 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
             const int ts = t0 + lt * kR;
             const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (ts + kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
             const int jb_hi = g.skip ? (L + g.off + g.zlead - ts + 31) / 32 : g.Kp / 32;
-            if (live) tile32<S, FUSED, false>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+            if (live) tile32<S, FUSED, false, 36>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
         } else {
             // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
             // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
             const int tw = t0 + (lt & ~31) * kR;
             const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
             const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
-            if (live) tile32<S, FUSED, use_antidiag<S, PROD>()>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+            if (live) tile32<S, FUSED, use_antidiag<S, PROD>(), 32>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
         }
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
@@ -353,7 +355,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     const int S = lead & 3, zlead = lead - S;
     g.Ke = static_cast<int>(K) + zlead;
     g.Kp = (g.Ke + 31) / 32 * 32;
-    g.Kpp = g.Kp / 32 * 36;
+    g.Kpp = g.Kp;  // the mirrored path (set below) stages taps at the window's pitch
     g.base_row = static_cast<int>((off + lead) / 32);
     g.off = static_cast<int>(off);
     g.zlead = zlead;
@@ -364,6 +366,7 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.TPR = NT / g.RPT;
     const int T = g.TPR * kR;
     g.mirror = g.skip && T >= L && 4 * K >= L && g.TPR % 64 == 0;
+    if (g.mirror) g.Kpp = g.Kp / 32 * 36;
     g.NR = T / 32 + g.Kp / 32 + (S >= 2 ? 1 : 0);  // S >= 2: 13-quad windows read 4 floats further
     if (g.NR <= 256) {
         g.nbox = 1;
@@ -389,8 +392,12 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     float* kp = nullptr;
     ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * g.Kpp, st));
     if (rc != KS_OK) return rc;
-    launch_kernel(prep_taps_pad36, static_cast<unsigned>(std::min<int64_t>((H * g.Kpp + 255) / 256, 4096)), 256, 0,
-                  st, k, kp, H, K, g.Kpp, reverse, zlead);
+    if (g.mirror)
+        launch_kernel(prep_taps_pad36, static_cast<unsigned>(std::min<int64_t>((H * g.Kpp + 255) / 256, 4096)), 256,
+                      0, st, k, kp, H, K, g.Kpp, reverse, zlead);
+    else
+        launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0, st,
+                      k, kp, H, K, g.Kp, reverse, zlead);
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;

@@ -150,7 +150,7 @@ def memory_traffic_rw(path: str, B: int, H: int, L: int, K: int, scheme: str = "
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
         staged = p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short", "stencil_ldg")
-        kp = 4 * H * (16 if p["kernel"] in ("stencil_short", "stencil_ldg") else math.ceil(K / 32) * 36)
+        kp = 4 * H * (16 if p["kernel"] in ("stencil_short", "stencil_ldg") else math.ceil(K / 32) * 32)
         return T + kb + (kp if staged else 0), T + (kp if staged else 0)
     if p["kernel"] == "dw_pairwise_tma":
         return 2 * T, kb
@@ -229,9 +229,10 @@ def _stencil_pad(B, H, L, K, off, occ):
     while rpt < 4 and nt * kr // (2 * rpt) >= L and H % (2 * rpt) == 0:
         rpt *= 2
     T = nt // rpt * kr
+    mirror = T >= L and 4 * K >= L and (nt // rpt) % 64 == 0  # the mirrored lane rings (K comparable to L)
     nr = T // 32 + Kp // 32 + (1 if S >= 2 else 0)
     nbox, nb = (1, nr) if nr <= 256 else (2, ((nr + 1) // 2 + 7) // 8 * 8)
-    Kpp = Kp // 32 * 36  # taps staged at the window's 36-float pitch per 32-tap block
+    Kpp = Kp // 32 * 36 if mirror else Kp  # mirrored: taps at the window's 36-float pitch per 32-tap block
     stage = _cdiv(rpt * nbox * nb * 36 * 4 + rpt * Kpp * 4, 1024) * 1024
     ns = 1 if K >= 1024 else 3
     while ns > 1 and ns * stage + 1152 > 110 * 1024:
@@ -239,7 +240,7 @@ def _stencil_pad(B, H, L, K, off, occ):
     smem = ns * stage + 128 + 1024
     threads = nt + (32 if K < 1024 else 0)
     tiles = B * H // rpt * _cdiv(L, T)
-    prep = _launch("prep_taps_pad36", min(_cdiv(H * Kpp, 256), 4096), 256, 0)
+    prep = _launch("prep_taps_pad36" if mirror else "prep_taps", min(_cdiv(H * Kpp, 256), 4096), 256, 0)
     return [prep, _launch("stencil_pad", min(tiles, SMS * occ(threads, smem)), threads, smem)]
 
 
