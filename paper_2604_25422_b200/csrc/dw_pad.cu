@@ -98,17 +98,27 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     if (tid >= kNT) {  // producer warp: one lane issues the loads, NS items ahead
         if (tid == kNT) {
             const uint32_t tx_bytes = static_cast<uint32_t>((g.gy_rows + g.nbx * g.NBX) * 144);
+            // stage / phase / (row, tile) carried incrementally: no integer
+            // divisions by the runtime NS and tile count per item
+            int stage = 0, b = b_begin, r0 = 0;
+            uint32_t phase = 0;
             for (int u = 0; u < nunits; ++u) {
-                const int stage = u % NS;
-                if (u >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((u / NS - 1) & 1));
-                const int b = b_begin + u / ntt;
-                const int r0 = (u % ntt) * (g.TT / 32);
+                if (u >= NS) mbar_wait_sleep(&empty[stage], phase ^ 1u);
                 unsigned char* sb = smem + stage * g.stage_bytes;
                 mbar_arrive_expect_tx(&full[stage], tx_bytes);
                 tma_load_pad(sb, &gy_map, r0, h, b, &full[stage]);
                 unsigned char* xb = sb + g.gy_alloc * 144;
                 tma_load_pad(xb, &x_map, r0 + xrow_rel, h, b, &full[stage]);
                 if (g.nbx > 1) tma_load_pad(xb + g.NBX * 144, &x_map, r0 + xrow_rel + g.NBX, h, b, &full[stage]);
+                r0 += g.TT / 32;
+                if (r0 * 32 >= L) {
+                    r0 = 0;
+                    ++b;
+                }
+                if (++stage == NS) {
+                    stage = 0;
+                    phase ^= 1u;
+                }
             }
         }
         return;
@@ -126,12 +136,12 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int ts_lo = LANE_JG ? ts : NTS >= 32 ? (tid & ~31) % NTS : 0;
     const int xw_lo = j0 + 32 * jgw - p + 32 * ts_lo;                         // + t0 of the chunk row
     const int xw_hi = j0 + 32 * (jgw + JGW) - 1 - p + 32 * (ts_lo + TSW) - 1;  // (chunk base i * NTS)
+    int stage = 0, tu = 0;
+    uint32_t phase = 0;
     for (int u = 0; u < nunits; ++u) {
-        const int stage = u % NS;
-        mbar_wait(&full[stage], static_cast<uint32_t>((u / NS) & 1));
+        mbar_wait(&full[stage], phase);
         const float* pg = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const float* px = pg + g.gy_alloc * 36;
-        const int tu = (u % ntt) * g.TT;
         for (int c = ts; c < nchunks; c += NTS) {
             // skip the chunk when, for the whole warp, every x it would read is
             // zero halo: gy * 0 never changes a sum that starts at +0 (and the
@@ -182,6 +192,12 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
             window(16);
         }
         mbar_arrive(&empty[stage]);  // this thread is done with the stage
+        if (++stage == NS) {
+            stage = 0;
+            phase ^= 1u;
+        }
+        tu += g.TT;
+        if (tu >= L) tu = 0;
     }
 
     // fixed-order reduction over the NTS t-slices of each tap group; the stage

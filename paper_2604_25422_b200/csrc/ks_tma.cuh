@@ -38,6 +38,21 @@ __device__ __forceinline__ float4 lds4(const void* p) {
     return v;
 }
 
+// 128-bit shared load from a 32-bit shared-window address.
+__device__ __forceinline__ float4 lds4_u32(uint32_t a) {
+    float4 v;
+    asm volatile("ld.shared.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+    return v;
+}
+
+// A per-thread value ptxas must keep in a register: without it ptxas may
+// rematerialise a thread's shared-window address inside the FMA loop from
+// SR_TID.X (an S2R + IMAD chain per window whose latency stalls the warp).
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t v) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(v));
+    return v;
+}
+
 // Pointer into the dynamic shared buffer rounded up to `align` bytes, derived
 // from the __shared__ array itself so the compiler keeps the shared address
 // space (LDS/STS rather than generic LD/ST).

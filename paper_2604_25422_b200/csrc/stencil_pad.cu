@@ -179,6 +179,59 @@ __device__ __forceinline__ void tile32(const float* pw, const float* wk, int pba
     }
 }
 
+// The warp-uniform variant of tile32 (every lane of the warp in the same
+// channel row with the same tap-block bounds): the tap addresses are provably
+// warp-uniform, so ptxas keeps each 16-tap window's taps in uniform registers
+// (LDS + R2UR) and, in anti-diagonal order, the shared window value sits in
+// the operand-reuse cache -- each FFMA reads only its accumulator from the
+// register file (no even/odd bank conflicts, tools/sass_banks.py ~1.03 per
+// FFMA against ~1.45 for tile32).  No tail special case: the staged taps are
+// zero-padded to Kp, a block's second window is skipped when all its taps
+// are padding, and a partially padded window multiplies in exact zeros (the
+// leading-zero argument above; trailing taps stay within the documented
+// non-finite contract).  Each register tile keeps the reference's ascending-j
+// chain from +0.
+template <int S, bool FUSED>
+__device__ __forceinline__ void tile32u(const float* pw, const float* wk, int pbase, int Ke, int jend, int jb_lo,
+                                        float (&acc)[kR]) {
+    constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) acc[r] = 0.f;
+    const uint32_t wbase = opaque_u32(smem_u32(pw + pbase));  // this thread's window, in a register
+    auto window = [&](const uint32_t base, const int sub, const float* w16) {
+        float v[4 * NV];
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const float4 q = lds4_u32(base + 4u * (sub + 4 * c + (((sub + 4 * c) >> 5) << 2)));
+            v[4 * c + 0] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+        float w[kJS];
+#pragma unroll
+        for (int c = 0; c < kJS / 4; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(w16 + 4 * c);
+            w[4 * c + 0] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+        }
+#pragma unroll
+        for (int m = 0; m < kR + kJS - 1; ++m)
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const int jj = m - r;
+                if (jj >= 0 && jj < kJS) acc[r] = muladd<FUSED>(acc[r], v[S + m], w[jj]);
+            }
+    };
+    for (int j0 = jb_lo * 32; j0 < jend; j0 += 32) {
+        const uint32_t b0 = wbase + static_cast<uint32_t>(j0 >> 5) * 144u;
+        window(b0, 0, wk + j0);
+        if (j0 + kJS < Ke) window(b0, 16, wk + j0 + 16);
+    }
+}
+
 // PROD: one extra warp whose lane 0 keeps the ring NS tiles ahead, and every
 // consumer thread releases a stage as soon as it is done with it (moderate K,
 // where tiles are short); !PROD: thread 0 refills a stage after a CTA barrier
@@ -227,6 +280,8 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
             int it = 0;
             for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
                 const int stage = it % NS;
+                // (parked: a spinning producer measured the same, and refilling
+                // from the last consumer warp to finish a stage 1-4% slower)
                 if (it >= NS) mbar_wait_sleep(&empty[stage], static_cast<uint32_t>((it / NS - 1) & 1));
                 issue(stage, tile);
             }
@@ -244,7 +299,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     // keeps RPT <= 4); where use_shfl() says so, rsub is broadcast from lane 0
     // so the compiler can prove the tap addresses warp-uniform and keep the
     // taps in uniform registers
-    const int rsub = use_shfl<S, PROD>() ? __shfl_sync(0xffffffffu, tid / g.TPR, 0) : tid / g.TPR;
+    const int rsub = (use_shfl<S, PROD>() || !LANEB) ? __shfl_sync(0xffffffffu, tid / g.TPR, 0) : tid / g.TPR;
     // lt: this thread's 32-output register tile within the channel row.  With
     // `mirror` (a tile spans the whole row and K is comparable to L, where an
     // output's valid tap count is ~ K - |t - L/2|), lane pairs take tiles
@@ -283,9 +338,14 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
             // the warp's outputs t in [tw, tw + 1024): tap block jb reads x at
             // t + 32 jb - zlead - off + [0, 32); keep the blocks that reach [0, L)
             const int tw = t0 + (lt & ~31) * kR;
-            const int jb_lo = g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
-            const int jb_hi = g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32;
-            if (live) tile32<S, FUSED, use_antidiag<S, PROD>(), 32>(pw_r, wk_r, lt * 36, g.Ke, jb_lo, jb_hi, acc);
+            // (broadcast from lane 0: equal on every lane, and provably uniform
+            // to ptxas, which then keeps the taps in uniform registers)
+            const int jb_lo = __shfl_sync(0xffffffffu,
+                                          g.skip ? max(0, (g.off + g.zlead - 31 - (tw + 32 * kR - 1) + 31 + 32 * 64) / 32 - 64) : 0, 0);
+            const int jb_hi = __shfl_sync(0xffffffffu, g.skip ? (L + g.off + g.zlead - tw + 31) / 32 : g.Kp / 32, 0);
+            // lanes past the row end compute on the stage's zero fill (their
+            // outputs are not stored): no divergent branch around the FFMAs
+            tile32u<S, FUSED>(pw_r, wk_r, lt * 36, g.Ke, min(g.Kp, 32 * jb_hi), jb_lo, acc);
         }
         if constexpr (PROD) {
             mbar_arrive(&empty[stage]);  // this thread is done with the stage
@@ -380,9 +440,11 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.win_floats = g.RPT * g.nbox * g.NB * 36;
     g.stage_bytes = (g.win_floats * 4 + g.RPT * g.Kpp * 4 + 1023) / 1024 * 1024;
     if (B * H / g.RPT * ((L + T - 1) / T) >= (int64_t(1) << 31)) return KS_OK;
-    // stages: two in flight beyond the one being computed while the CTA count
-    // per SM stays >= 2; long K (>= 1024) computes ~100x longer than it loads
-    int NS = K >= 1024 ? 1 : 3;
+    // stages: one in flight beyond the one being computed (a tile computes
+    // ~10x longer than its load takes to land; two stages leave room for a
+    // fourth CTA per SM, measured 1-1.5% faster than three at K = 128 / 256);
+    // long K (>= 1024) computes ~100x longer than it loads: one stage
+    int NS = K >= 1024 ? 1 : 2;
     while (NS > 1 && pad_smem(g, NS) > 110 * 1024) --NS;
     if (opt(kOptPadNs) > 0) NS = static_cast<int>(std::min<int64_t>(4, opt(kOptPadNs)));
     if (pad_smem(g, NS) > 220 * 1024) return KS_OK;

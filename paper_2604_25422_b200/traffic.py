@@ -234,7 +234,7 @@ def _stencil_pad(B, H, L, K, off, occ):
     nbox, nb = (1, nr) if nr <= 256 else (2, ((nr + 1) // 2 + 7) // 8 * 8)
     Kpp = Kp // 32 * 36 if mirror else Kp  # mirrored: taps at the window's 36-float pitch per 32-tap block
     stage = _cdiv(rpt * nbox * nb * 36 * 4 + rpt * Kpp * 4, 1024) * 1024
-    ns = 1 if K >= 1024 else 3
+    ns = 1 if K >= 1024 else 2
     while ns > 1 and ns * stage + 1152 > 110 * 1024:
         ns -= 1
     smem = ns * stage + 128 + 1024

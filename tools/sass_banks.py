@@ -7,7 +7,11 @@ source operand held in the operand-reuse cache (the previous instruction set
 .reuse on the same slot with the same register) is not read from the RF.
 Prints, per function, #FFMA and the modelled FFMA issue cycles.
 
-usage: python tools/sass_banks.py file.sass [more.sass ...]
+With --blocks, also prints every basic block (split at branches and branch
+targets) holding >= 64 FFMAs: its FFMA count, ratio, and the share of its
+instructions that are FFMAs (the issue-slot ceiling of the FMA pipe there).
+
+usage: python tools/sass_banks.py [--blocks] file.sass [more.sass ...]
 """
 import re
 import sys
@@ -48,22 +52,59 @@ def analyse(lines):
     return n, cyc, hist
 
 
+def blocks(lines):
+    """Basic blocks of one function: split after branches / exits and before branch targets."""
+    targets = set()
+    for ln in lines:
+        m = INS.search(ln)
+        if m and "BRA" in m.group(3):
+            t = re.search(r"0x([0-9a-f]+)", m.group(4))
+            if t:
+                targets.add(int(t.group(1), 16))
+    out, cur = [], []
+    for ln in lines:
+        m = INS.search(ln)
+        if not m:
+            continue
+        if int(m.group(1), 16) in targets and cur:
+            out.append(cur)
+            cur = []
+        cur.append(ln)
+        if m.group(3).startswith(("BRA", "EXIT", "RET", "JMP")):
+            out.append(cur)
+            cur = []
+    if cur:
+        out.append(cur)
+    return out
+
+
 def main():
-    for path in sys.argv[1:]:
+    args = sys.argv[1:]
+    per_block = "--blocks" in args
+    args = [a for a in args if a != "--blocks"]
+    for path in args:
         fn, buf = None, []
-        out = []
+        out, bufs = [], {}
         for ln in open(path):
             if "Function :" in ln:
                 if fn:
                     out.append((fn, analyse(buf)))
+                    bufs[fn] = buf
                 fn, buf = ln.split("Function :")[1].strip(), []
             else:
                 buf.append(ln)
         if fn:
             out.append((fn, analyse(buf)))
+            bufs[fn] = buf
         for fn, (n, cyc, hist) in out:
             if n:
                 print(f"{fn[:90]}\n   FFMA {n}  modelled issue cycles {cyc}  ratio {cyc / n:.3f}  hist {sorted(hist.items())}")
+            if per_block:
+                for b in blocks(bufs[fn]):
+                    bn, bc, _ = analyse(b)
+                    if bn >= 64:
+                        addr = INS.search(b[0]).group(1)
+                        print(f"     block @{addr}: {len(b)} instr, FFMA {bn} ({bn / len(b):.1%}), ratio {bc / bn:.3f}")
 
 
 if __name__ == "__main__":

@@ -14,7 +14,7 @@ def main():
     rows = list(csv.reader(open(sys.argv[1])))
     thr = float(sys.argv[2]) if len(sys.argv) > 2 else 0.005
     kernel = rows[0][1] if len(rows[0]) > 1 else "?"
-    hdr, data = rows[1], rows[2:]
+    hdr, data = rows[1], [r for r in rows[2:] if r and r[0] != "Address"]
     i_s = hdr.index("Warp Stall Sampling (All Samples)")
     i_e = hdr.index("Instructions Executed")
     sc = [i for i, h in enumerate(hdr) if h.startswith("stall_") and "Not Issued" not in h]
