@@ -105,6 +105,7 @@ enum Opt {
     kOptStencilNt,
     kOptStencilNs,
     kOptHostBlockMb,
+    kOptStencilBl,
     kOptCount
 };
 int64_t opt(Opt o);

@@ -42,6 +42,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"stencil_nt", 0, 0, 1024},  // stencil_tma threads (0: auto)
     {"stencil_ns", 0, 0, 8},     // stencil_tma stages (0: auto)
     {"host_block_mb", 64, 1, 4096},  // host-buffer entry points: bytes per streamed block
+    {"stencil_bl", -1, -1, 1},   // stencil_pad's batch-lane kernel: 1 always, 0 never, -1 auto (K >= L / 4)
 };
 
 std::atomic<int64_t> g_opts[kOptCount];

@@ -364,6 +364,191 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     }
 }
 
+// ---------------------------------------------------------------------------
+// Batch-lane stencil (K comparable to L, e.g. config 2's K = L): the lanes of
+// a warp are 32 batch rows of ONE channel at the SAME 32 outputs, so every
+// lane has the same taps (uniform registers), the same valid tap blocks (no
+// zero-halo waste beyond the 32-tap block granularity, no lane divergence)
+// and warps need no per-tile barrier.  CTA = (channel h, 32 batch rows,
+// 4 x 32 outputs); warp c owns outputs [t0 + 32 c, +32) of the 32 rows.
+// The input streams through a ring of one-piece slots: slot = 32 rows x one
+// padded 32-float piece (box {36, 1, 1, 32} of the padded view, rows 144 B
+// apart -- conflict-free 128-bit lane reads), loaded in ascending piece order
+// by one producer lane; tap block jb of warp c reads pieces Q = ts/32 -
+// base_row + jb, Q + 1 (and Q + 2 when S >= 2), so consecutive blocks reuse a
+// piece and each warp releases a piece once it is past it (per-thread arrives
+// on the slot's empty barrier).  Taps: the CTA's prepared row (prep_taps,
+// `lead` zeros) bulk-loaded once.  Bits: each output's chain is tile32u's
+// (ascending j from +0, zero taps / zero fill exact for finite inputs).
+constexpr int kBlNW = 4;                  // consumer warps = output columns of 32
+constexpr int kBlSlots = 8;               // ring slots (pieces; 12 slots, or taps read from L1 to make room, measured 1-2% slower)
+constexpr int kBlSlotBytes = 32 * 144;    // 32 rows x one padded piece
+
+struct BlGeom {
+    int Kp, Ke, base_row, off, zlead, skip;
+    int ncol, ngrp;  // output tiles of 128 per row, groups of 32 batch rows
+};
+
+__device__ __forceinline__ void bl_bounds(const BlGeom& g, int L, int ts, int& lo, int& hi) {
+    if (ts >= L) {
+        lo = 0;
+        hi = 0;
+        return;
+    }
+    lo = g.skip ? max(0, (g.off + g.zlead - 31 - (ts + kR - 1) + 31 + 32 * 64) / 32 - 64) : 0;
+    hi = min(g.Kp / 32, g.skip ? (L + g.off + g.zlead - ts + 31) / 32 : g.Kp / 32);
+}
+
+template <int S, bool FUSED>
+__global__ void __launch_bounds__(kNT + 32)
+stencil_bl(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out, int B,
+           int H, int L, BlGeom g) {
+    constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
+    constexpr int XP = S >= 2 ? 2 : 1;  // pieces past Q a block reads
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = align_smem<1024>(smem_raw);
+    unsigned char* slots = smem;
+    float* taps = reinterpret_cast<float*>(smem + kBlSlots * kBlSlotBytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + kBlSlots * kBlSlotBytes + g.Kp * 4);
+    uint64_t* empty = full + kBlSlots;
+    uint64_t* tapbar = empty + kBlSlots;
+
+    const int bid = static_cast<int>(blockIdx.x);
+    const int col = bid % g.ncol, rest = bid / g.ncol;
+    const int grp = rest % g.ngrp, h = rest / g.ngrp;
+    const int t0 = col * kBlNW * kR, b0 = grp * 32;
+    // the CTA's piece range: the union of its warps' blocks (all uniform)
+    int pfirst = 1 << 30, plast = -(1 << 30);
+#pragma unroll
+    for (int c = 0; c < kBlNW; ++c) {
+        int lo, hi;
+        bl_bounds(g, L, t0 + c * kR, lo, hi);
+        if (lo < hi) {
+            const int q0 = (t0 + c * kR) / 32 - g.base_row;
+            pfirst = min(pfirst, q0 + lo);
+            plast = max(plast, q0 + hi - 1 + XP);
+        }
+    }
+    const int npieces = plast >= pfirst ? plast - pfirst + 1 : 0;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        prefetch_tmap(&in_map);
+        for (int s = 0; s < kBlSlots; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kNT);
+        }
+        mbar_init(tapbar, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+
+    if (tid >= kNT) {  // producer warp: lane 0 streams the pieces
+        if (tid == kNT) {
+            mbar_arrive_expect_tx(tapbar, static_cast<uint32_t>(g.Kp) * 4u);
+            bulk_load(taps, kp + static_cast<int64_t>(h) * g.Kp, static_cast<uint32_t>(g.Kp) * 4u, tapbar);
+            int slot = 0;
+            uint32_t phase = 0;
+            for (int i = 0; i < npieces; ++i) {
+                if (i >= kBlSlots) mbar_wait_sleep(&empty[slot], phase ^ 1u);
+                mbar_arrive_expect_tx(&full[slot], kBlSlotBytes);
+                tma_load_pad(slots + slot * kBlSlotBytes, &in_map, pfirst + i, h, b0, &full[slot]);
+                if (++slot == kBlSlots) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
+        }
+        return;
+    }
+
+    const int warp = tid >> 5, lane = tid & 31;
+    const int ts = t0 + warp * kR;
+    int jb_lo, jb_hi;
+    bl_bounds(g, L, ts, jb_lo, jb_hi);
+    jb_lo = __shfl_sync(0xffffffffu, jb_lo, 0);  // provably uniform to ptxas
+    jb_hi = __shfl_sync(0xffffffffu, jb_hi, 0);
+    const int q0 = __shfl_sync(0xffffffffu, ts / 32 - g.base_row, 0);
+    const uint32_t lrow = opaque_u32(smem_u32(slots) + static_cast<uint32_t>(lane) * 144u);
+    mbar_wait(tapbar, 0);
+
+    float acc[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) acc[r] = 0.f;
+    // one 16-tap window: quads at logical sub + 4c of the block's pieces
+    auto window = [&](const uint32_t (&pb)[3], const int sub, const float* w16) {
+        float v[4 * NV];
+#pragma unroll
+        for (int c = 0; c < NV; ++c) {
+            const int e = sub + 4 * c;
+            const float4 q = lds4_u32(pb[e >> 5] + 4u * (e & 31));
+            v[4 * c + 0] = q.x;
+            v[4 * c + 1] = q.y;
+            v[4 * c + 2] = q.z;
+            v[4 * c + 3] = q.w;
+        }
+        float w[kJS];
+#pragma unroll
+        for (int c = 0; c < kJS / 4; ++c) {
+            const float4 q = *reinterpret_cast<const float4*>(w16 + 4 * c);
+            w[4 * c + 0] = q.x;
+            w[4 * c + 1] = q.y;
+            w[4 * c + 2] = q.z;
+            w[4 * c + 3] = q.w;
+        }
+#pragma unroll
+        for (int m = 0; m < kR + kJS - 1; ++m)
+#pragma unroll
+            for (int r = 0; r < kR; ++r) {
+                const int jj = m - r;
+                if (jj >= 0 && jj < kJS) acc[r] = muladd<FUSED>(acc[r], v[S + m], w[jj]);
+            }
+    };
+    int slot = 0;
+    uint32_t phase = 0;
+    for (int i = 0; i < npieces; ++i) {
+        mbar_wait(&full[slot], phase);
+        const int jb = pfirst + i - q0;  // the block whose first piece is this one
+        if (jb >= jb_lo && jb < jb_hi) {
+            uint32_t pb[3];
+            pb[0] = lrow + static_cast<uint32_t>(slot * kBlSlotBytes);
+#pragma unroll
+            for (int x = 1; x <= XP; ++x) {
+                const int sx = slot + x >= kBlSlots ? slot + x - kBlSlots : slot + x;
+                const uint32_t px = slot + x >= kBlSlots ? phase ^ 1u : phase;
+                mbar_wait(&full[sx], px);
+                pb[x] = lrow + static_cast<uint32_t>(sx * kBlSlotBytes);
+            }
+            if (XP == 1) pb[2] = pb[1];
+            const int j0 = jb * 32;
+            window(pb, 0, taps + j0);
+            if (j0 + kJS < g.Ke) window(pb, 16, taps + j0 + 16);
+        }
+        mbar_arrive(&empty[slot]);  // this thread is past the piece
+        if (++slot == kBlSlots) {
+            slot = 0;
+            phase ^= 1u;
+        }
+    }
+    if (ts < L && b0 + lane < B) {
+        float* o = out + (static_cast<int64_t>(b0 + lane) * H + h) * L + ts;
+#pragma unroll
+        for (int r = 0; r < kR; r += 4) st_cs_v4(o + r, make_float4(acc[r], acc[r + 1], acc[r + 2], acc[r + 3]));
+    }
+}
+
+int bl_smem(const BlGeom& g) { return kBlSlots * kBlSlotBytes + g.Kp * 4 + 256 + 1024; }
+
+template <int S, bool FUSED>
+ks_status launch_bl(const CUtensorMap& im, const float* kp, float* out, int64_t B, int64_t H, int64_t L,
+                    const BlGeom& g, cudaStream_t st) {
+    auto kern = stencil_bl<S, FUSED>;
+    const int smem = bl_smem(g);
+    prepare_kernel(reinterpret_cast<const void*>(kern), kNT + 32, smem);
+    launch_kernel(kern, static_cast<unsigned>(int64_t(g.ncol) * g.ngrp * H), kNT + 32, smem, st, im, kp, out,
+                  static_cast<int>(B), static_cast<int>(H), static_cast<int>(L), g);
+    return check_launch();
+}
+
 int pad_smem(const PadGeom& g, int NS) { return NS * g.stage_bytes + 128 + 1024; }
 
 template <int S, bool FUSED, bool PROD>
@@ -420,6 +605,42 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     g.off = static_cast<int>(off);
     g.zlead = zlead;
     g.skip = opt(kOptPadSkip) != 0;
+    // batch-lane kernel: K comparable to L (the per-lane tap ranges of the
+    // row-tile kernel diverge there), at least one full warp of batch rows
+    const int64_t bl_opt = opt(kOptStencilBl);
+    if (bl_opt != 0 && B >= 32 && (bl_opt > 0 || 4 * K >= L) && B * H < (int64_t(1) << 31)) {
+        BlGeom bg{};
+        bg.Kp = g.Kp;
+        bg.Ke = g.Ke;
+        bg.base_row = g.base_row;
+        bg.off = g.off;
+        bg.zlead = g.zlead;
+        bg.skip = g.skip;
+        bg.ncol = static_cast<int>((L + kBlNW * kR - 1) / (kBlNW * kR));
+        bg.ngrp = static_cast<int>((B + 31) / 32);
+        CUtensorMap bm;
+        if (bl_smem(bg) <= 200 * 1024 && int64_t(bg.ncol) * bg.ngrp * H < (int64_t(1) << 31) &&
+            encode_padded_view(&bm, in, B * H, L, H, 1, 1, 32)) {
+            float* kpb = nullptr;
+            ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kpb), sizeof(float) * H * g.Kp, st));
+            if (rc != KS_OK) return rc;
+            launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * g.Kp + 255) / 256, 4096)), 256, 0,
+                          st, k, kpb, H, K, int64_t(g.Kp), reverse, zlead);
+            rc = check_launch();
+            if (rc == KS_OK) {
+                const bool fused = mode == KS_MULADD_FUSED;
+                switch (S) {
+                    case 0: rc = fused ? launch_bl<0, true>(bm, kpb, out, B, H, L, bg, st) : launch_bl<0, false>(bm, kpb, out, B, H, L, bg, st); break;
+                    case 1: rc = fused ? launch_bl<1, true>(bm, kpb, out, B, H, L, bg, st) : launch_bl<1, false>(bm, kpb, out, B, H, L, bg, st); break;
+                    case 2: rc = fused ? launch_bl<2, true>(bm, kpb, out, B, H, L, bg, st) : launch_bl<2, false>(bm, kpb, out, B, H, L, bg, st); break;
+                    default: rc = fused ? launch_bl<3, true>(bm, kpb, out, B, H, L, bg, st) : launch_bl<3, false>(bm, kpb, out, B, H, L, bg, st); break;
+                }
+            }
+            scratch_free(kpb, st);
+            *handled = true;
+            return rc;
+        }
+    }
     g.mirror = 0;  // set below, once the tile width is known
     g.RPT = 1;
     while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;

@@ -70,11 +70,13 @@ def logical_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
     return 8 * B * H * L + 4 * H * K
 
 
-def _stencil_tier(L: int, K: int):
+def _stencil_tier(L: int, K: int, B: int = 1):
     if L < 1024 and L % 4 == 0 and L + K - 1 <= 252:
         return "stencil_rows", 16, None
     if L % 32 != 0 or K > 8192:
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
+    if K > 32 and L >= 1024 and B >= 32 and 4 * K >= L:
+        return "stencil_bl", 32, 128  # batch lanes: 32 rows x 128 outputs per CTA + 1 producer lane
     if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
     if K <= 8 and L >= 1024:
@@ -122,7 +124,10 @@ def plan(path: str, B: int, H: int, L: int, K: int, scheme: str = "hierarchical"
             return {"kernel": "bwd_short", "row_groups": G, "partials_bytes": 4 * G * H * K}
         return {"kernel": "split", "dx": plan("dx", B, H, L, K), "dw": plan("dw", B, H, L, K)}
     if path in ("fwd", "dx"):
-        name, R, NT = _stencil_tier(L, K)
+        name, R, NT = _stencil_tier(L, K, B)
+        if name == "stencil_bl":  # a tile = 32 batch rows x 128 outputs of one channel
+            return {"kernel": name, "R": R, "threads": NT, "outputs_per_tile": 32 * 128,
+                    "tiles": math.ceil(B / 32) * H * math.ceil(L / 128)}
         T = (NT or 0) * R if NT else None
         tiles = B * H * math.ceil(L / T) if T else None
         return {"kernel": name, "R": R, "threads": NT, "outputs_per_tile": T, "tiles": tiles}
@@ -149,7 +154,7 @@ def memory_traffic_rw(path: str, B: int, H: int, L: int, K: int, scheme: str = "
         return 2 * T + kb + p["partials_bytes"], T + p["partials_bytes"] + kb
     p = plan(path, B, H, L, K, scheme)
     if path in ("fwd", "dx"):
-        staged = p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_short", "stencil_ldg")
+        staged = p["kernel"] in ("stencil_tma", "stencil_pad", "stencil_bl", "stencil_short", "stencil_ldg")
         kp = 4 * H * (16 if p["kernel"] in ("stencil_short", "stencil_ldg") else math.ceil(K / 32) * 32)
         return T + kb + (kp if staged else 0), T + (kp if staged else 0)
     if p["kernel"] == "dw_pairwise_tma":
@@ -184,6 +189,8 @@ def halo_bytes(path: str, B: int, H: int, L: int, K: int) -> int:
         lead = (32 - off % 32) % 32
         Kp = _cdiv(K + lead - (lead & 3), 32) * 32
         return B * H * _cdiv(L, 4096) * (Kp + 32) * 4
+    if p["kernel"] == "stencil_bl":  # every CTA streams its pieces: the 128 outputs' valid window
+        return sum(n * 32 * 128 for n in _bl_pieces(B, H, L, K, off)) * _cdiv(B, 32) * H - 4 * B * H * L
     if not p["tiles"]:
         return 0
     HH = 1 if p["kernel"] == "stencil_short" else max(1, math.ceil(max(off, K - 1 - off) / 32))
@@ -242,6 +249,43 @@ def _stencil_pad(B, H, L, K, off, occ):
     tiles = B * H // rpt * _cdiv(L, T)
     prep = _launch("prep_taps_pad36" if mirror else "prep_taps", min(_cdiv(H * Kpp, 256), 4096), 256, 0)
     return [prep, _launch("stencil_pad", min(tiles, SMS * occ(threads, smem)), threads, smem)]
+
+
+def _bl_geom(K, off):
+    lead = (32 - off % 32) % 32
+    S, zlead = lead & 3, lead - (lead & 3)
+    Kp = _cdiv(K + zlead, 32) * 32
+    return S, zlead, Kp, (off + lead) // 32
+
+
+def _bl_pieces(B, H, L, K, off):
+    """Pieces each CTA of one row group and channel streams, per output column
+    tile (stencil_bl's union of its four warps' valid tap blocks)."""
+    S, zlead, Kp, base_row = _bl_geom(K, off)
+    xp = 2 if S >= 2 else 1
+    out = []
+    for col in range(_cdiv(L, 128)):
+        lo_p, hi_p = None, None
+        for c in range(4):
+            ts = col * 128 + 32 * c
+            if ts >= L:
+                continue
+            lo = max(0, (off + zlead - 31 - (ts + 31) + 31 + 32 * 64) // 32 - 64)
+            hi = min(Kp // 32, (L + off + zlead - ts + 31) // 32)
+            if lo < hi:
+                q0 = ts // 32 - base_row
+                lo_p = q0 + lo if lo_p is None else min(lo_p, q0 + lo)
+                hi_p = q0 + hi - 1 + xp if hi_p is None else max(hi_p, q0 + hi - 1 + xp)
+        out.append(0 if lo_p is None else hi_p - lo_p + 1)
+    return out
+
+
+def _stencil_bl(B, H, L, K, off):
+    """stencil_pad.cu BlGeom: 4 consumer warps + a producer, an 8-slot ring of
+    32-row pieces, the channel's prepared taps staged once."""
+    _, _, Kp, _ = _bl_geom(K, off)
+    smem = 8 * 32 * 144 + Kp * 4 + 256 + 1024
+    return [_prep_taps(H, Kp), _launch("stencil_bl", _cdiv(L, 128) * _cdiv(B, 32) * H, 160, smem)]
 
 
 def _dw_pad(B, H, L, K, G):
@@ -332,6 +376,8 @@ def launch_geometry(path: str, B: int, H: int, L: int, K: int, scheme: str = "hi
             return [_prep_taps(H, 16), _bwd_short(path, B, H, L, K, 1, occ)]
         if kind == "stencil_pad":
             return _stencil_pad(B, H, L, K, off, occ)
+        if kind == "stencil_bl":
+            return _stencil_bl(B, H, L, K, off)
         if kind == "stencil_rows":
             return [_stencil_rows(B, H, L, K, off, occ)]
         raise NotImplementedError(kind)

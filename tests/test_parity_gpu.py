@@ -323,6 +323,32 @@ def test_padded_view_kernels_many_tiles(oracle, shape):
             assert normwise(dk[h:h + 1], truth) <= HIER_TOL
 
 
+@pytest.mark.parametrize("shape", [(32, 3, 4096, 4096), (40, 2, 2048, 700), (64, 2, 1024, 257),
+                                   (33, 2, 2080, 1000), (32, 4, 2048, 33), (96, 1, 4096, 1030)])
+def test_batch_lane_stencil_bitwise(oracle, shape):
+    """stencil_pad's batch-lane kernel (lanes = 32 batch rows of one channel at
+    the same outputs; the default where K >= L / 4): y and dX bitwise against
+    the oracle on sampled channels (every batch row, incl. a ragged last group
+    of rows when B % 32 != 0, a ragged last output tile at L = 2080, all four
+    sub-quad offsets), forced on, in both modes -- and bitwise equal to the
+    row-tile kernel (stencil_bl=0)."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(5, B, H, L, K)
+    kh = k.cpu().numpy()
+    for m in (SEPARATE, FUSED):
+        with ks.options(stencil_bl=1):
+            y = ks.forward(x, k, m)
+            dx = ks.backward_input(gy, k, m)
+        with ks.options(stencil_bl=0):
+            assert same(host(y), host(ks.forward(x, k, m))), m
+            assert same(host(dx), host(ks.backward_input(gy, k, m))), m
+        for h in sorted({0, H - 1}):
+            xs, gs = _channel_slice(x, h), _channel_slice(gy, h)
+            ks_ = np.ascontiguousarray(kh[h:h + 1])
+            assert same(_channel_slice(y, h), oracle.forward(xs, ks_, m)), (h, m)
+            assert same(_channel_slice(dx, h), oracle.backward_input(gs, ks_, m)), (h, m)
+
+
 @pytest.mark.parametrize("shape", [(3, 4, 2048, 7), (2, 3, 4096, 8), (5, 2, 2080, 16), (4, 3, 3072, 9),
                                    (2, 2, 2048, 1), (16, 8, 2048, 13), (1, 1, 2048, 2), (40, 16, 2048, 7),
                                    (2, 2, 1024, 7), (2, 2, 2048, 40)])

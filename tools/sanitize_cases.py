@@ -47,8 +47,11 @@ for (B, H, L, K) in shapes:
 # more rows than CTAs), dW and fused backward with ragged last tiles
 # (2,4,4096,4096), (3,8,1024,1024): K comparable to L -> stencil_pad's mirrored,
 # rotating lane rings with per-lane zero-halo bounds
+# (40,2,2048,1030), (32,3,1024,700): K comparable to L with >= 32 batch rows ->
+# the batch-lane stencil (piece ring wraps several times, ragged row group, S = 1..3)
 for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48),
-                     (40, 16, 2080, 16), (8, 4, 4160, 13), (2, 4, 4096, 4096), (3, 8, 1024, 1024)]:
+                     (40, 16, 2080, 16), (8, 4, 4160, 13), (2, 4, 4096, 4096), (3, 8, 1024, 1024),
+                     (40, 2, 2048, 1030), (32, 3, 1024, 700)]:
     x, k, gy = o.fill_inputs(5, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
     y = ks.forward(dx_, dk_, 1)
