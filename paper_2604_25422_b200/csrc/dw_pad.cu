@@ -138,8 +138,10 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int xw_hi = j0 + 32 * (jgw + JGW) - 1 - p + 32 * (ts_lo + TSW) - 1;  // (chunk base i * NTS)
     int stage = 0, tu = 0;
     uint32_t phase = 0;
+    // barrier addresses in registers (not re-derived from SR_CgaCtaId per item)
+    const uint32_t full_u = opaque_u32(smem_u32(full)), empty_u = full_u + 8u * NS;
     for (int u = 0; u < nunits; ++u) {
-        mbar_wait(&full[stage], phase);
+        mbar_wait_u32(full_u + 8u * stage, phase);
         const float* pg = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const float* px = pg + g.gy_alloc * 36;
         for (int c = ts; c < nchunks; c += NTS) {
@@ -191,7 +193,7 @@ dw_pad(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
             window(0);
             window(16);
         }
-        mbar_arrive(&empty[stage]);  // this thread is done with the stage
+        mbar_arrive_u32(empty_u + 8u * stage);  // this thread is done with the stage
         if (++stage == NS) {
             stage = 0;
             phase ^= 1u;

@@ -99,6 +99,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// The same on a 32-bit shared address held in a register (hot loops: keeps
+// ptxas from re-deriving the barrier's shared-window address per iteration).
+__device__ __forceinline__ void mbar_wait_u32(uint32_t bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "KS_WAITU_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra KS_WAITU_%=;\n"
+        "}\n" ::"r"(bar),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+
 // Parked wait for a producer lane: try_wait with a suspend-time hint blocks
 // the thread in hardware until the phase completes (or ~1 ms passes), so the
 // producer takes no issue slots from the FMA warps it feeds.  (The previous

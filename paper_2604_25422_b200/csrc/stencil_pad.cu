@@ -312,6 +312,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
     const int q = tid - rsub * g.TPR;
     const int nwr = g.TPR / 32;
     const int win_rows = g.nbox * g.NB;
+    const uint32_t full_u = opaque_u32(smem_u32(full)), empty_u = full_u + 8u * NS;
     int it = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int stage = it % NS;
@@ -319,7 +320,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
         const int lt = !LANEB ? q
                               : ((q & 1) ? g.TPR / 2 + 16 * ring + ((q & 31) >> 1)
                                          : g.TPR / 2 - 1 - 16 * ring - ((q & 31) >> 1));
-        mbar_wait(&full[stage], static_cast<uint32_t>((it / NS) & 1));
+        mbar_wait_u32(full_u + 8u * stage, static_cast<uint32_t>((it / NS) & 1));
         const float* sw = reinterpret_cast<const float*>(smem + stage * g.stage_bytes);
         const int rg = tile / tiles_per_row;
         const int t0 = (tile - rg * tiles_per_row) * T;
@@ -348,7 +349,7 @@ stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict_
             tile32u<S, FUSED>(pw_r, wk_r, lt * 36, g.Ke, min(g.Kp, 32 * jb_hi), jb_lo, acc);
         }
         if constexpr (PROD) {
-            mbar_arrive(&empty[stage]);  // this thread is done with the stage
+            mbar_arrive_u32(empty_u + 8u * stage);  // this thread is done with the stage
         } else {
             __syncthreads();  // stage consumed by every thread
             if (tid == 0) {
@@ -505,8 +506,9 @@ stencil_bl(const __grid_constant__ CUtensorMap in_map, const float* __restrict__
     };
     int slot = 0;
     uint32_t phase = 0;
+    const uint32_t full_u = opaque_u32(smem_u32(full)), empty_u = full_u + 8u * kBlSlots;
     for (int i = 0; i < npieces; ++i) {
-        mbar_wait(&full[slot], phase);
+        mbar_wait_u32(full_u + 8u * slot, phase);
         const int jb = pfirst + i - q0;  // the block whose first piece is this one
         if (jb >= jb_lo && jb < jb_hi) {
             uint32_t pb[3];
@@ -515,7 +517,7 @@ stencil_bl(const __grid_constant__ CUtensorMap in_map, const float* __restrict__
             for (int x = 1; x <= XP; ++x) {
                 const int sx = slot + x >= kBlSlots ? slot + x - kBlSlots : slot + x;
                 const uint32_t px = slot + x >= kBlSlots ? phase ^ 1u : phase;
-                mbar_wait(&full[sx], px);
+                mbar_wait_u32(full_u + 8u * sx, px);
                 pb[x] = lrow + static_cast<uint32_t>(sx * kBlSlotBytes);
             }
             if (XP == 1) pb[2] = pb[1];
@@ -523,7 +525,7 @@ stencil_bl(const __grid_constant__ CUtensorMap in_map, const float* __restrict__
             window(pb, 0, taps + j0);
             if (j0 + kJS < g.Ke) window(pb, 16, taps + j0 + 16);
         }
-        mbar_arrive(&empty[slot]);  // this thread is past the piece
+        mbar_arrive_u32(empty_u + 8u * slot);  // this thread is past the piece
         if (++slot == kBlSlots) {
             slot = 0;
             phase ^= 1u;
