@@ -433,8 +433,28 @@ def run_ours(args, cfg_name, cfg):
     if not graphs:
         for fn in set(split_fns + step_fns):
             launches[fn] = count(fn)
+    # the whole step (forward, then the backward) as ONE graph as well: a
+    # training loop replays its step once, so the step time below carries one
+    # graph launch, not one per path (config 1: ~8 us per replay)
+    step_graph = None
+    if graphs:
+        try:
+            step_graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(step_graph):
+                for fn in step_fns:
+                    fn()
+        except Exception as exc:
+            print(f"bench.py: whole-step graph capture failed ({exc}); the step time uses per-path graphs",
+                  file=sys.stderr)
+            step_graph = None
     torch.cuda.synchronize()
     play = {fn: (graphs[fn].replay if fn in graphs else fn) for fn in set(split_fns + step_fns)}
+
+    def run_step():
+        step_graph.replay()
+
+    if step_graph is not None:
+        play[run_step] = run_step
 
     def combine():
         if comm is not None and peer is None:
@@ -480,6 +500,8 @@ def run_ours(args, cfg_name, cfg):
 
     per_split, ms_split_total = timed(split_fns, True)
     per_step, ms_total = (per_split, ms_split_total) if not fused_bwd else timed(step_fns, True)
+    if step_graph is not None:  # the step time proper: one replay of the whole step per step
+        _, ms_total = timed([run_step], True)
     clk.__exit__(None, None, None)
     split_mean = per_split.mean(axis=0)  # fwd, dX, dW, combine
     step_mean = per_step.mean(axis=0)    # fwd, bwd (or dX, dW), combine
@@ -589,7 +611,8 @@ def run_ours(args, cfg_name, cfg):
     # our kernels launched inside the two timed loops (counted by the library
     # at capture / launch time: ks_launch_count)
     gpu_launches = args.steps * (sum(launches[f] for f in split_fns) +
-                                 (sum(launches[f] for f in step_fns) if fused_bwd else 0))
+                                 (sum(launches[f] for f in step_fns) if fused_bwd else 0) +
+                                 (sum(launches[f] for f in step_fns) if step_graph is not None else 0))
 
     # ---- end to end from pinned host memory (H2D / D2H inside the timed region) ----
     e2e = e2e_step = None
@@ -680,6 +703,8 @@ def run_ours(args, cfg_name, cfg):
                     "l2": "inputs larger than L2 (no flush)" if flush is None
                           else "L2 flushed before every timed step (512 MB write, untimed)",
                     "cuda_graphs": bool(graphs),
+                    "step_timing": "one CUDA-graph replay per step (fwd + bwd)" if step_graph is not None
+                                   else "per-path launches",
                     "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)",
                     "frac_hbm_measured": round(value / world / peak, 4), "frac_hbm_8TBs": round(value / world / 8000, 4)},
             "paths": paths,

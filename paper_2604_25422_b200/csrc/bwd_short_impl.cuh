@@ -20,7 +20,8 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
     auto kern = bwd_short<KT, FUSED, MODE>;
     constexpr int smem = Geo<KT, MODE>::Smem;
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
-    const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
+    const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H
+                           : opt(kOptStsRows) ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
     launch_kernel(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
                                                                 static_cast<int>(H), static_cast<int>(L), G, out);
     return check_launch();

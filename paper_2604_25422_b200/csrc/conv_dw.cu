@@ -174,8 +174,19 @@ template <typename T>
 __global__ void dw_sum_groups(const T* __restrict__ part, T* __restrict__ dk, int64_t HK, int G) {
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= HK) return;
+    // ascending g, plain adds; the loads of a block of 8 groups are issued
+    // before its adds (independent), so the chain waits on memory once per
+    // 8 groups, not once per group (config 1: G = 16, 5.2 -> ~1.5 us)
     T s = part[i];
-    for (int g = 1; g < G; ++g) s += part[static_cast<int64_t>(g) * HK + i];
+    int g = 1;
+    for (; g + 8 <= G; g += 8) {
+        T v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = part[static_cast<int64_t>(g + u) * HK + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) s += v[u];
+    }
+    for (; g < G; ++g) s += part[static_cast<int64_t>(g) * HK + i];
     dk[i] = s;
 }
 
@@ -362,13 +373,20 @@ struct HierPlan {
     int g;    // row groups
 };
 
-HierPlan hier_plan(int64_t B, int64_t H, int64_t K) {
+// CTA target: dw_ctas (8192 by default) -- but never so many that a CTA holds
+// less than ~2^18 multiply-adds: small problems (config 1: 67 M MACs) are
+// latency-bound per CTA, and fewer, fuller CTAs amortise the per-CTA tile
+// loads and reduction trees (config 1 dW 12.3 -> 10.0 us at 256 CTAs instead
+// of 1024; `tools/sweep_options.py`, gpurun_out/s5).  Large shapes are
+// unaffected (the paper's shape wants its 8192).
+HierPlan hier_plan(int64_t B, int64_t H, int64_t L, int64_t K) {
     HierPlan pl;
     const int64_t groups8 = (K + kJR - 1) / kJR;
     pl.nj = 1;
     while (pl.nj < 8 && pl.nj < groups8) pl.nj *= 2;
     pl.njt = static_cast<int>((K + pl.nj * kJR - 1) / (pl.nj * kJR));
-    const int64_t target = 8192;
+    const double macs = static_cast<double>(B) * H * L * K;
+    const int64_t target = std::min<int64_t>(opt(kOptDwCtas), std::max<int64_t>(256, static_cast<int64_t>(macs / 262144.0)));
     int64_t g = (target + H * pl.njt - 1) / (H * pl.njt);
     g = std::max<int64_t>(1, std::min<int64_t>(g, B));
     pl.g = static_cast<int>(g);
@@ -431,14 +449,14 @@ ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B,
 // Row groups G of the HIERARCHICAL partial buffer part[G,H,K] for this shape.
 static int hier_groups(int64_t B, int64_t H, int64_t L, int64_t K) {
     if (!tma_disabled() && dw_pad_applies(B, H, L, K)) return dw_pad_groups(B, H, K);
-    return hier_plan(B, H, K).g;
+    return hier_plan(B, H, L, K).g;
 }
 
 size_t dw_workspace_bytes(int64_t B, int64_t H, int64_t L, int64_t K, int scheme, int64_t chunk,
                           int elem) {
     if (scheme == KS_DW_HIERARCHICAL) {
         if (elem != 4) return 0;  // fp64 HIERARCHICAL runs the exact pairwise kernel
-        const int g = std::max(hier_groups(B, H, L, K), hier_plan(B, H, K).g);
+        const int g = std::max(hier_groups(B, H, L, K), hier_plan(B, H, L, K).g);
         return size_t(g) * H * K * sizeof(float);
     }
     if (scheme == KS_DW_PAIRWISE) return elem == 4 ? dw_pairwise_tma_workspace(B, H, L, K) : 0;
@@ -543,13 +561,13 @@ ks_status dw_stage1_only(const float* gy, const float* x, float* part, int64_t B
         scratch_free(a, st);
         return s;
     }
-    HierPlan pl = hier_plan(B, H, K);
+    HierPlan pl = hier_plan(B, H, L, K);
     bool handled = false;
     ks_status s = KS_OK;
     if (!tma_disabled() && dw_pad_applies(B, H, L, K)) {  // compute-bound long K (dw_pad.cu)
         pl.g = G_req > 0 ? G_req : dw_pad_groups(B, H, K);
         s = dw_pad_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);
-        if (!handled) pl = hier_plan(B, H, K);
+        if (!handled) pl = hier_plan(B, H, L, K);
     }
     if (G_req > 0) pl.g = G_req;
     if (!handled && L < 2048) s = dw_rows_stage1(gy, x, part, B, H, L, K, pl.g, mode, st, &handled);  // short rows
@@ -574,7 +592,7 @@ ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* 
     // unaligned bases: the split path (dw_f32 stages them into aligned scratch)
     if (((reinterpret_cast<uintptr_t>(gy) | reinterpret_cast<uintptr_t>(x)) & 15) != 0) return KS_OK;
     if (L > (1ll << 30) || B > (1ll << 30)) return KS_OK;
-    const HierPlan pl = hier_plan(B, H, K);
+    const HierPlan pl = hier_plan(B, H, L, K);
     float* part = static_cast<float*>(ws);
     const ks_status s = bwd_tma_stage1(gy, x, k, dx, part, B, H, L, K, pl.g, mode, st, fused);
     if (s != KS_OK || !*fused) return s;

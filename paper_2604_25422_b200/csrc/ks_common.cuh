@@ -106,6 +106,8 @@ enum Opt {
     kOptStencilNs,
     kOptHostBlockMb,
     kOptStencilBl,
+    kOptDwCtas,
+    kOptStsRows,
     kOptCount
 };
 int64_t opt(Opt o);

@@ -112,7 +112,11 @@ ks_status launch_any(int64_t K, bool fused, const float* in, const float4* kp, f
 
 // *handled = false when the shape / alignment is outside this kernel's
 // envelope (L % 8 == 0, 16-byte input and 32-byte output bases) or the knob
-// says otherwise.  Default: K <= 8.  Measured on the B200 (bench.py, ABAB):
+// says otherwise.  Default: K <= 10 (round-2 ABAB
+// sweep over K = 9..16 at (256,512,8192,K), tools/sweep_options.py,
+// gpurun_out/s5: K = 9 fwd 1.45 -> 1.25 ms Fused, 1.50 -> 1.32 Separate;
+// K = 10 Fused 1.46 -> 1.36, Separate even; K >= 11 the TMA kernels win,
+// Separate mode by up to 25% at K = 16).  Measured on the B200 (bench.py, ABAB):
 // config 3 (K = 7) fwd 1.40 -> 1.22 ms and dX 1.42 -> 1.22 ms (7.0 TB/s),
 // but config 5a (K = 16, (512,1024,16384)) fwd 11.5 -> 13.3 and dX 11.2 ->
 // 14.1 ms under the power cap (at (256,512,8192,16) it was 4% faster), so the
@@ -122,7 +126,7 @@ ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B
                           int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
     const int knob = static_cast<int>(opt(kOptLdg));
-    if (knob == 0 || K > (knob >= 2 ? 16 : 8)) return KS_OK;
+    if (knob == 0 || K > (knob >= 2 ? 16 : 10)) return KS_OK;
     if (K < 1 || K > 16 || L % 8 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;
     if ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 31) != 0) return KS_OK;

@@ -79,7 +79,7 @@ def _stencil_tier(L: int, K: int, B: int = 1):
         return "stencil_bl", 32, 128  # batch lanes: 32 rows x 128 outputs per CTA + 1 producer lane
     if K > 32 and L >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
-    if K <= 8 and L >= 1024:
+    if K <= 10 and L >= 1024:
         return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if K <= 16 and L >= 1024:
         return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
@@ -102,7 +102,8 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
     while nj < 8 and nj < groups8:
         nj *= 2
     njt = math.ceil(K / (nj * 8))
-    G = max(1, min(math.ceil(8192 / (H * njt)), B))
+    target = min(8192, max(256, (B * H * L * K) // 262144))  # conv_dw.cu hier_plan: >= 2^18 MACs per CTA
+    G = max(1, min(math.ceil(target / (H * njt)), B))
     if L < 2048 and L % 4 == 0 and L + 8 * min(8, groups8) + 16 <= 252:  # dw_rows: a whole row in one TMA box
         return "dw_rows", G
     if L % 32 == 0 and K <= 16:

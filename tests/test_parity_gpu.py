@@ -390,7 +390,7 @@ def test_bwd_short_equals_generic_kernels(K):
 @pytest.mark.parametrize("K", list(range(1, 17)))
 def test_stencil_short_equals_generic_and_oracle(K, oracle):
     """The three short-kernel forward / dX implementations -- register windows
-    with 256-bit stores (stencil_ldg, the default for K <= 8, forced for every
+    with 256-bit stores (stencil_ldg, the default for K <= 10, forced for every
     K by option ldg=2), the K-specialised TMA kernel (bwd_short.cuh, ldg=0;
     persistent grid with more rows than CTAs) and the generic stencil_tma
     (ldg=0 sts=0) -- bit for bit against

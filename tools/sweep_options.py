@@ -44,6 +44,8 @@ def main():
     ap.add_argument("--mode", choices=["separate", "fused"], default="separate")
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--reps", type=int, default=7)
+    ap.add_argument("--graph", action="store_true", help="time CUDA-graph replays of --inner calls (small shapes)")
+    ap.add_argument("--inner", type=int, default=20, help="calls per graph replay with --graph")
     a = ap.parse_args()
     mode = ks.FUSED if a.mode == "fused" else ks.SEPARATE
     shapes = [tuple(int(v) for v in s.split()) for s in a.shapes.split(";")]
@@ -62,7 +64,17 @@ def main():
             for s in sets:
                 with ks.options(**parse_set(s)):
                     for p in paths:
-                        res.setdefault((shape, p, s), []).append(timed(fns[p], a.reps))
+                        if a.graph:  # options are read at capture time
+                            fns[p]()
+                            torch.cuda.synchronize()
+                            g = torch.cuda.CUDAGraph()
+                            with torch.cuda.graph(g):
+                                for _ in range(a.inner):
+                                    fns[p]()
+                            ms = timed(g.replay, a.reps) / a.inner
+                        else:
+                            ms = timed(fns[p], a.reps)
+                        res.setdefault((shape, p, s), []).append(ms)
         del x, k, gy, y, dx
         torch.cuda.empty_cache()
     print(f"mode {a.mode}; median ms over {a.rounds} ABAB rounds")
