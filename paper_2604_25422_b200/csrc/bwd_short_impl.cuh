@@ -20,8 +20,15 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
     auto kern = bwd_short<KT, FUSED, MODE>;
     constexpr int smem = Geo<KT, MODE>::Smem;
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
+    // stencils: a persistent grid in Separate mode (issue-bound: two FP
+    // instructions per tap), one CTA per row in Fused mode, where an item is
+    // short and the hardware scheduler's rebalancing of many CTAs pays
+    // (round-2 ABAB, gpurun_out/s8: (64,1024,16384,16) fwd 1.50 -> 1.27 ms,
+    // config 5a fwd 11.8 -> 10.9 ms; Separate 1-9% slower with it)
+    const int64_t rows_opt = opt(kOptStsRows);
+    const bool per_row = rows_opt == 1 || (rows_opt < 0 && FUSED);
     const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H
-                           : opt(kOptStsRows) ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
+                           : per_row ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
     launch_kernel(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
                                                                 static_cast<int>(H), static_cast<int>(L), G, out);
     return check_launch();

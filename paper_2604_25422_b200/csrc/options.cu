@@ -44,7 +44,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"host_block_mb", 64, 1, 4096},  // host-buffer entry points: bytes per streamed block
     {"stencil_bl", -1, -1, 1},   // stencil_pad's batch-lane kernel: 1 always, 0 never, -1 auto (K >= L / 4)
     {"dw_ctas", 8192, 64, 1 << 20},
-    {"sts_rows", 0, 0, 1},       // bwd_short stencils: one CTA per row (1) instead of a persistent grid (0)  // HIERARCHICAL stage 1 (dw_tma / bwd_short / dw_rows / generic): target CTAs (sets G)
+    {"sts_rows", -1, -1, 1},     // bwd_short stencils: one CTA per row (1), persistent grid (0), -1 auto (rows in Fused mode)  // HIERARCHICAL stage 1 (dw_tma / bwd_short / dw_rows / generic): target CTAs (sets G)
 };
 
 std::atomic<int64_t> g_opts[kOptCount];

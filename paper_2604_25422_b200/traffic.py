@@ -223,6 +223,8 @@ def _bwd_short(mode: str, B, H, L, K, G, occ):
     stage = gy_region + (x_region if has_dw else 0) + (128 if mode in ("fwd", "dx") else 0)
     ns = 4 if mode in ("fwd", "dx") else (4 if K <= 8 else 3)
     smem = (2 * 8192 if has_st else 0) + ns * stage + 64 + 1024
+    # stencils: persistent in Separate mode (the plans and this model are for
+    # Separate, the reference's default); Fused mode launches one CTA per row
     grid = G * H if has_dw else min(B * H, SMS * occ(256, smem))
     return _launch("bwd_short", grid, 256, smem)
 
