@@ -37,7 +37,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"pad_ns", 0, 0, 4},         // stencil_pad stages (0: auto)
     {"pad_prod", -1, -1, 1},     // stencil_pad producer lane (1) or CTA-barrier refill (0); -1 auto
     {"dwpad_ns", 0, 0, 4},       // dw_pad stages (0: auto)
-    {"stencil_pad", 1, 0, 1},    // compute-bound K > 32 fwd/dX through stencil_pad (0: stencil_tma R=32)
+    {"stencil_pad", 1, 0, 2},    // K > 32 fwd/dX through stencil_pad: 0 never (stencil_tma), 1 auto (not Separate K < 1024), 2 always
     {"stencil_r", 0, 0, 32},     // stencil_tma register tile (0: auto, 32: R = 32 at short K)
     {"stencil_nt", 0, 0, 1024},  // stencil_tma threads (0: auto)
     {"stencil_ns", 0, 0, 8},     // stencil_tma stages (0: auto)

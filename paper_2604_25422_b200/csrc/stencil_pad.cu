@@ -643,6 +643,12 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
             return rc;
         }
     }
+    // Separate mode below K = 1024: the R = 32 register-tile kernel of
+    // stencil_tma.cu is faster (two FP instructions per tap; round-2 ABAB,
+    // gpurun_out/s10: config 4 fwd 9.50 -> 8.95 ms, dX 9.13 -> 8.93, 5b shard
+    // fwd 10.01 -> 9.57), Fused mode and K >= 1024 keep this kernel (Fused
+    // config 4 fwd 4.35 vs 5.80 ms).  Option stencil_pad = 2 forces it.
+    if (mode != KS_MULADD_FUSED && K < 1024 && opt(kOptStencilPad) < 2) return KS_OK;
     g.mirror = 0;  // set below, once the tile width is known
     g.RPT = 1;
     while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;

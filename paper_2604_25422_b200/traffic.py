@@ -77,12 +77,17 @@ def _stencil_tier(L: int, K: int, B: int = 1):
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
     if K > 32 and L >= 1024 and B >= 32 and 4 * K >= L:
         return "stencil_bl", 32, 128  # batch lanes: 32 rows x 128 outputs per CTA + 1 producer lane
-    if K > 32 and L >= 1024:
+    if K > 32 and L >= 1024 and K >= 1024:
         return "stencil_pad", 32, 128  # padded TMA view, 128 FMA threads + 1 producer lane
+    # Separate mode (the reference's default, which this model and the committed
+    # plans follow) below K = 1024: stencil_tma's register tiles (Fused mode
+    # takes stencil_pad here too)
     if K <= 10 and L >= 1024:
         return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if K <= 16 and L >= 1024:
         return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
+    if K > 32 and L >= 2048:  # stencil_tma.cu pick_tile
+        return "stencil_tma", 32, 256 if L >= 8192 else 128 if L >= 4096 else 64
     if L >= 1024:
         nt = 256 if L >= 4096 and K <= 8 else 128 if L >= 2048 else 64
         return "stencil_tma", 16, nt
@@ -254,6 +259,29 @@ def _stencil_pad(B, H, L, K, off, occ):
     return [prep, _launch("stencil_pad", min(tiles, SMS * occ(threads, smem)), threads, smem)]
 
 
+def _stencil_tma(B, H, L, K, off, R, NT, occ):
+    """stencil_tma.cu StencilGeom: NT threads x R outputs per tile, a window of
+    128-byte rows with HH halo rows each side, taps at Kp = ceil(K/32)*32."""
+    T = NT * R
+    mr = T // 32
+    hh = max(1, _cdiv(max(off, K - 1 - off), 32))
+    w = mr + 2 * hh
+    nbox, nb = (1, w) if w <= 256 else (2, w // 2)
+    kp = _cdiv(K, 32) * 32
+    stage = _cdiv(nbox * nb * 128 + kp * 4, 1024) * 1024
+    out_bytes = _cdiv(T * 4, 1024) * 1024
+    tma_out = R != 32
+    smem_of = lambda n: n * stage + (2 * out_bytes if tma_out else 0) + 64 + 1024  # noqa: E731
+    ns = 2 if K > 8 else 3
+    while ns > 2 and smem_of(ns) > 110 * 1024:
+        ns -= 1
+    if R == 32:
+        ns = 1 if K >= 1024 else 2
+    smem = smem_of(ns)
+    tiles = B * H * _cdiv(L, T)
+    return [_prep_taps(H, kp), _launch("stencil_tma", min(tiles, SMS * occ(NT, smem)), NT, smem)]
+
+
 def _bl_geom(K, off):
     lead = (32 - off % 32) % 32
     S, zlead = lead & 3, lead - (lead & 3)
@@ -383,6 +411,8 @@ def launch_geometry(path: str, B: int, H: int, L: int, K: int, scheme: str = "hi
             return _stencil_bl(B, H, L, K, off)
         if kind == "stencil_rows":
             return [_stencil_rows(B, H, L, K, off, occ)]
+        if kind == "stencil_tma":
+            return _stencil_tma(B, H, L, K, off, pl["R"], pl["threads"], occ)
         raise NotImplementedError(kind)
     kind, G = pl["kernel"], pl.get("row_groups")
     tail = [_launch("dw_sum_groups", _cdiv(H * K, 256), 256, 0)]

@@ -305,13 +305,16 @@ def test_padded_view_kernels_many_tiles(oracle, shape):
     """Compute-bound kernels fed by the padded TMA view (stencil_pad, dw_pad)
     with several tiles / work items per CTA, so every stage and both mbarrier
     phases recur (and RPT = 2 channels per tile at L = 2048): sampled channels
-    bitwise (y, dX) in both modes, dW to tolerance and run-to-run deterministic."""
+    bitwise (y, dX) in both modes, dW to tolerance and run-to-run deterministic.
+    Separate mode below K = 1024 defaults to stencil_tma's R = 32 tiles, so it
+    also runs with stencil_pad forced (option stencil_pad = 2)."""
     B, H, L, K = shape
     x, k, gy = ks.make_inputs(3, B, H, L, K)
     kh = k.cpu().numpy()
-    for m in (SEPARATE, FUSED):
-        y = ks.forward(x, k, m)
-        dx = ks.backward_input(gy, k, m)
+    for m, opts in ((SEPARATE, {}), (SEPARATE, {"stencil_pad": 2}), (FUSED, {})):
+        with ks.options(**opts):
+            y = ks.forward(x, k, m)
+            dx = ks.backward_input(gy, k, m)
         dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
         assert same(dk, host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m)))
         for h in (0, H // 3, H - 1):
@@ -456,9 +459,10 @@ def test_short_rows_many_chunks(oracle, shape):
     B, H, L, K = shape
     x, k, gy = ks.make_inputs(4, B, H, L, K)
     kh = k.cpu().numpy()
-    for m in (SEPARATE, FUSED):
-        y = ks.forward(x, k, m)
-        dx = ks.backward_input(gy, k, m)
+    for m, opts in ((SEPARATE, {}), (SEPARATE, {"stencil_pad": 2}), (FUSED, {})):
+        with ks.options(**opts):
+            y = ks.forward(x, k, m)
+            dx = ks.backward_input(gy, k, m)
         dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, m))
         for h in (0, H // 2, H - 1):
             xs, gs = _channel_slice(x, h), _channel_slice(gy, h)

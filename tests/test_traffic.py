@@ -22,7 +22,9 @@ def test_plan_dispatch_tiers():
     assert traffic.plan("fwd", 512, 1024, 16384, 16)["kernel"] == "stencil_short"
     assert traffic.plan("fwd", 64, 128, 4096, 4096)["kernel"] == "stencil_bl"  # K >= L / 4, B >= 32
     assert traffic.plan("fwd", 16, 128, 4096, 4096)["kernel"] == "stencil_pad"  # fewer than 32 rows
-    assert traffic.plan("fwd", 1024, 256, 2048, 256)["kernel"] == "stencil_pad"
+    # the model follows Separate mode (the reference's default): register tiles below K = 1024
+    assert traffic.plan("fwd", 1024, 256, 2048, 256)["kernel"] == "stencil_tma"
+    assert traffic.plan("fwd", 512, 1024, 16384, 1024)["kernel"] == "stencil_pad"
     assert traffic.plan("fwd", 16384, 128, 48, 48)["kernel"] == "stencil_rows"
     assert traffic.plan("dw", 64, 128, 4096, 4096)["kernel"] == "dw_pad"
     assert traffic.plan("dw", 256, 512, 8192, 7)["kernel"] == "dw_short"

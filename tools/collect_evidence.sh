@@ -22,6 +22,7 @@ done
 for t in memcheck racecheck synccheck; do [ -s $O/sanitize_$t.log ] && tail -n 3 $O/sanitize_$t.log > $P/r02_sanitize_$t.log; done
 [ -s $O/pytest_gpu.log ] && tail -n 2 $O/pytest_gpu.log > $P/r02_pytest_gpu.log
 [ -s $O/smoke.log ] && cp $O/smoke.log $P/r02_smoke.log
+[ -s $O/hbm_mix.log ] && (echo "# tools/probes/hbm_mix_probe.cu (tools/gpu_evidence.sh): HBM streaming rate per read:write mix"; cat $O/hbm_mix.log) > $P/r02_hbm_mix.txt
 # the reference's own analysis pipeline over the ablation logs (oracle/_ref/ks_b200_report)
 if [ -x oracle/_ref/ks_b200_report ]; then
   for l in $P/r02_ablation_*_paper.csv $P/r02_ablation_*_library.csv; do

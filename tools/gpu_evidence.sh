@@ -6,6 +6,8 @@ T="timeout 900"
 $T python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 python tools/dump_plans.py $O/plans.json > $O/plans.log 2>&1
 python tools/b200_device_spec.py $O/b200_device_spec.json > $O/spec.log 2>&1
+# HBM streaming rate per read:write mix (the roof each HBM-bound path is judged against)
+[ -x tools/probes/hbm_mix_probe ] && timeout 120 tools/probes/hbm_mix_probe > $O/hbm_mix.log 2>&1
 # bench lines: the headline (config 3, Separate = the reference's default, e2e + CPU baseline), then every config in both modes
 $T python bench.py > $O/bench_config3.json 2> $O/bench_config3.err
 $T python bench.py --impl reference > $O/bench_reference_config3.json 2> $O/bench_reference_config3.err
