@@ -233,8 +233,12 @@ static void pick_tile(int64_t L, int64_t K, int* R, int* NT) {
         *R = 16;
         *NT = L >= 4096 && K <= 8 ? 256 : L >= 2048 ? 128 : 64;
     } else {
+        // short rows the row kernels cannot take (L + K too long for one box):
+        // the smallest tile that still covers a row, so a tile is not mostly
+        // past the row end ((4096,128,256,32): T = 1024 left 3/4 of every
+        // tile empty)
         *R = 4;
-        *NT = 256;
+        *NT = L > 512 ? 256 : L > 256 ? 128 : L > 128 ? 64 : 32;
     }
 }
 
@@ -318,7 +322,10 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
     rc = check_launch();
     if (rc == KS_OK) {
         const bool fused = mode == KS_MULADD_FUSED;
-        if (R == 4) rc = launch_s<4, 256>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
+        if (R == 4 && NT == 256) rc = launch_s<4, 256>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
+        else if (R == 4 && NT == 128) rc = launch_s<4, 128>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
+        else if (R == 4 && NT == 64) rc = launch_s<4, 64>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
+        else if (R == 4) rc = launch_s<4, 32>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
         else if (R == 16 && NT == 256) rc = launch_s<16, 256>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
         else if (R == 16 && NT == 128) rc = launch_s<16, 128>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);
         else if (R == 16) rc = launch_s<16, 64>(s, fused, im, om, kp, out, B, H, L, K, g, NS, st);

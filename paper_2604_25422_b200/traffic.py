@@ -91,7 +91,7 @@ def _stencil_tier(L: int, K: int, B: int = 1):
     if L >= 1024:
         nt = 256 if L >= 4096 and K <= 8 else 128 if L >= 2048 else 64
         return "stencil_tma", 16, nt
-    return "stencil_tma", 4, 256
+    return "stencil_tma", 4, 256 if L > 512 else 128 if L > 256 else 64 if L > 128 else 32
 
 
 def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:

@@ -417,6 +417,22 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
             assert same(_channel_slice(dx, h), oracle.backward_input(_channel_slice(gy, h), ks_, m)), (h, m)
 
 
+@pytest.mark.parametrize("shape", [(24, 8, 256, 32), (12, 8, 512, 300), (10, 6, 768, 40), (16, 4, 128, 200),
+                                   (8, 4, 992, 1000), (6, 5, 64, 500)])
+def test_mid_length_rows_register_tiles(oracle, shape):
+    """Rows shorter than 1024 whose L + K is too long for the whole-row
+    kernels (stencil_rows): stencil_tma's R = 4 tiles sized to the row
+    (32..256 threads), y and dX bitwise against the oracle in both modes,
+    every channel."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(21, B, H, L, K)
+    xh, gh, kh = host(x), host(gy), host(k)
+    for m in (SEPARATE, FUSED):
+        y, dx = host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))
+        assert same(y, oracle.forward(xh, kh, m)), m
+        assert same(dx, oracle.backward_input(gh, kh, m)), m
+
+
 @pytest.mark.parametrize("K", [1, 4, 7, 10, 13, 16])
 def test_short_kernels_both_output_paths(K):
     """The short-kernel stencils and fused backward write their outputs either
