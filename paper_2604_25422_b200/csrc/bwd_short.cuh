@@ -63,6 +63,9 @@ constexpr int kFUSED = 1;   // dX + dW stage 1 from one pass over gy and x
 constexpr int kFWD = 2;     // forward stencil: out = x (*) k, offset p
 constexpr int kDXS = 3;     // dX stencil: out = gy (*) reversed k, offset q
 constexpr int kDirect = 8;  // | kDirect: stencil outputs go straight to HBM (one 256-bit store per 8 outputs)
+constexpr int kMRow = 16;   // | kMRow (dW, L < 2048): an item is RPI whole rows of the CTA's channel, not one
+                            //   2048-wide tile of one row (the tile would be mostly past the row end)
+constexpr int kMaxRPI = 8;  // rows per multi-row item (L >= 256)
 
 constexpr int kThreads = 256;
 constexpr int kTT = 2048;                // t per work item
@@ -75,6 +78,7 @@ template <int KT, int MODE>
 struct Geo {
     static constexpr int BASE = MODE & 7;             // kDW / kFUSED / kFWD / kDXS
     static constexpr bool DST = (MODE & kDirect) != 0;  // stencil output stored straight from registers
+    static constexpr bool MR = (MODE & kMRow) != 0;     // multi-row dW items
     static constexpr bool HAS_DW = BASE <= kFUSED;  // x window + dW accumulators
     static constexpr bool HAS_ST = BASE >= kFUSED;  // a stencil output tile per item
     static constexpr int p = KT / 2;
@@ -91,8 +95,11 @@ struct Geo {
     static constexpr int GYP = BASE == kDW ? 64 : 66;     // stencil input: one halo piece each side
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
     static constexpr int TapBytes = BASE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
-    static constexpr int Stage = GYRegion + (HAS_DW ? kXRegion : 0) + TapBytes;
+    // multi-row items: each row's x window carries its own two halo pieces
+    static constexpr int XRegion = MR ? ((64 + 2 * kMaxRPI) * kPitch + 127) / 128 * 128 : kXRegion;
+    static constexpr int Stage = GYRegion + (HAS_DW ? XRegion : 0) + TapBytes;
     static constexpr int NS = BASE >= kFWD ? KS_ST_NS
+                              : MR ? 3
                               : KT <= 8 ? (BASE == kFUSED ? KS_FUSED_NS_SHORT : KS_DW_NS_SHORT)
                                         : KS_DW_NS_LONG;  // dW as dw_tma: 4 stages when FMAs are light
     static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : 3;
@@ -121,6 +128,8 @@ struct Args {
     int row0, rstep, nrows;  // this CTA's rows: row0 + i * rstep, i < nrows (row = b * H + h)
     int h;                   // dW modes: the CTA's channel
     int grp;                 // dW modes: the CTA's row group
+    int npr, rpi;            // multi-row dW: pieces per row (L / 32), rows per item
+    uint32_t tx;             // multi-row dW: bytes per item (both boxes)
 };
 
 // One work item's math for the thread whose block starts at column C0 of its
@@ -128,7 +137,8 @@ struct Args {
 // [base + imm]); the caller switches on the warp-uniform column around this
 // call only, so all warps meet the same barrier instructions.
 template <int KT, bool FUSED, int MODE, int C0>
-__device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob, uint32_t o0, uint32_t o1, float* gout,
+__device__ __forceinline__ void item(const unsigned char* gys, int xshift, unsigned char* ob, uint32_t o0, uint32_t o1,
+                                     float* gout,
                                      const float (&w)[Geo<KT, MODE>::HAS_ST ? 16 : 1],
                                      float (&acc)[Geo<KT, MODE>::HAS_DW ? KT : 1]) {
     using Gm = Geo<KT, MODE>;
@@ -174,7 +184,7 @@ __device__ __forceinline__ void item(const unsigned char* gys, unsigned char* ob
     }
     if constexpr (Gm::HAS_DW) {
         // dW: x logical (origin t0 - p - D) A + tl + 4c; acc[jj] += gy[t] * x[t + jj - p]
-        const unsigned char* xs = gys + Gm::GYRegion;
+        const unsigned char* xs = gys + Gm::GYRegion + (Gm::MR ? xshift : 0);
         float xv[4 * Gm::NVX];
 #pragma unroll
         for (int c = 0; c < Gm::NVX; ++c) {
@@ -200,7 +210,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     const int tid = threadIdx.x;
     const int warp = tid >> 5, lane = tid & 31;
     const int ntt = (a.L + kTT - 1) / kTT;
-    const int nunits = a.nrows * ntt;
+    const int nunits = Gm::MR ? (a.nrows + a.rpi - 1) / a.rpi : a.nrows * ntt;
     unsigned char* stages = smem + (Gm::HAS_OBUF ? 2 * kOutBytes : 0);
 
     // producer state (thread 0): next item to load
@@ -208,6 +218,17 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     auto issue = [&](int stage) {
         uint64_t* bar = &full[stage];
         unsigned char* sb = stages + stage * Gm::Stage;
+        if constexpr (Gm::MR) {
+            // RPI rows b .. b + RPI - 1 of channel h from the {32, L/32, H, B}
+            // padded view: gy as NPR pieces per row, x as NPR + 2 pieces from
+            // piece -XR0 (each row's own zero-filled halo)
+            mbar_arrive_expect_tx(bar, a.tx);
+            const int b = irow / a.H;
+            tma_load_pad(sb, in_map, 0, a.h, b, bar);
+            tma_load_pad(sb + Gm::GYRegion, x_map, -Gm::XR0, a.h, b, bar);
+            irow += a.rpi * a.rstep;
+            return;
+        }
         mbar_arrive_expect_tx(bar, Gm::TX);
 #if KS_EVICT_FIRST
         const uint64_t pol = policy_evict_first();
@@ -241,6 +262,10 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
 
     const int R = lane + 32 * (warp >> 2);  // piece of this thread's block within the tile
     const unsigned char* tb = stages + R * kPitch;
+    // multi-row items: piece R is piece q of row ri of the item (gy rows packed,
+    // x rows NPR + 2 pieces apart)
+    const int ri = Gm::MR ? R / a.npr : 0;
+    const int xshift = Gm::MR ? 2 * ri * kPitch : 0;
     const int cw = warp & 3;                // the block's column is 8 cw
     // output tile: 128B-swizzled rows of 32 floats, this thread's 8 outputs at row R, quads 2 cw, 2 cw + 1
     const uint32_t o0 = static_cast<uint32_t>(R * 128 + (((2 * cw) ^ (R & 7)) << 4));
@@ -263,13 +288,14 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
                 w[4 * c + 3] = qv.w;
             }
         }
-        if (t0 + 32 * R < a.L) {
+        const bool live = Gm::MR ? ri < min(a.rpi, a.nrows - u * a.rpi) : t0 + 32 * R < a.L;
+        if (live) {
             float* gout = Gm::DST ? a.out + static_cast<int64_t>(row) * a.L + t0 + 32 * R + 8 * cw : nullptr;
             switch (cw) {
-                case 0: item<KT, FUSED, MODE, 0>(gys, ob, o0, o1, gout, w, acc); break;
-                case 1: item<KT, FUSED, MODE, 8>(gys, ob, o0, o1, gout, w, acc); break;
-                case 2: item<KT, FUSED, MODE, 16>(gys, ob, o0, o1, gout, w, acc); break;
-                default: item<KT, FUSED, MODE, 24>(gys, ob, o0, o1, gout, w, acc); break;
+                case 0: item<KT, FUSED, MODE, 0>(gys, xshift, ob, o0, o1, gout, w, acc); break;
+                case 1: item<KT, FUSED, MODE, 8>(gys, xshift, ob, o0, o1, gout, w, acc); break;
+                case 2: item<KT, FUSED, MODE, 16>(gys, xshift, ob, o0, o1, gout, w, acc); break;
+                default: item<KT, FUSED, MODE, 24>(gys, xshift, ob, o0, o1, gout, w, acc); break;
             }
         }
         if constexpr (Gm::HAS_OBUF) {
@@ -334,7 +360,7 @@ template <int KT, bool FUSED, int MODE>
 __global__ void __launch_bounds__(kThreads, Geo<KT, MODE>::MinBlocks)  // 3 CTAs/SM (<= 80 regs), stencils 4
 bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap x_map,
           const __grid_constant__ CUtensorMap out_map, const float* __restrict__ k, float* __restrict__ part, int B,
-          int H, int L, int G, float* __restrict__ out) {
+          int H, int L, int G, float* __restrict__ out, int rpi) {
     using Gm = Geo<KT, MODE>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
@@ -344,6 +370,9 @@ bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CU
     a.H = H;
     a.L = L;
     a.out = out;
+    a.npr = L / 32;
+    a.rpi = rpi;
+    a.tx = static_cast<uint32_t>(rpi * (2 * a.npr + 2) * kPitch);
     if constexpr (Gm::HAS_DW) {
         a.h = blockIdx.x % H;
         a.grp = blockIdx.x / H;

@@ -16,7 +16,7 @@ namespace bwds {
 
 template <int KT, bool FUSED, int MODE>
 ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k, float* part,
-                   int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st) {
+                   int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st, int rpi = 0) {
     auto kern = bwd_short<KT, FUSED, MODE>;
     constexpr int smem = Geo<KT, MODE>::Smem;
     const int per_sm = prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);
@@ -30,15 +30,15 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
     const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H
                            : per_row ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
     launch_kernel(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
-                                                                static_cast<int>(H), static_cast<int>(L), G, out);
+                                                                static_cast<int>(H), static_cast<int>(L), G, out, rpi);
     return check_launch();
 }
 
 template <int KT, int MODE>
 ks_status launch_m(bool fused, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om, const float* k,
-                   float* part, int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st) {
+                   float* part, int64_t B, int64_t H, int64_t L, int G, float* out, cudaStream_t st, int rpi = 0) {
     // dW only: HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
-    if constexpr ((MODE & 7) == kDW) return launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
+    if constexpr ((MODE & 7) == kDW) return launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st, rpi);
     else
         return fused ? launch_k<KT, true, MODE>(im, xm, om, k, part, B, H, L, G, out, st)
                      : launch_k<KT, false, MODE>(im, xm, om, k, part, B, H, L, G, out, st);
@@ -47,10 +47,10 @@ ks_status launch_m(bool fused, const CUtensorMap& im, const CUtensorMap& xm, con
 template <int MODE>
 ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om,
                        const float* k, float* part, int64_t B, int64_t H, int64_t L, int G, float* out,
-                       cudaStream_t st) {
+                       cudaStream_t st, int rpi = 0) {
     switch (K) {
 #define KS_BWDS_CASE(KV) \
-    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, out, st);
+    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, out, st, rpi);
         KS_BWDS_CASE(1) KS_BWDS_CASE(2) KS_BWDS_CASE(3) KS_BWDS_CASE(4) KS_BWDS_CASE(5) KS_BWDS_CASE(6)
         KS_BWDS_CASE(7) KS_BWDS_CASE(8) KS_BWDS_CASE(9) KS_BWDS_CASE(10) KS_BWDS_CASE(11) KS_BWDS_CASE(12)
         KS_BWDS_CASE(13) KS_BWDS_CASE(14) KS_BWDS_CASE(15) KS_BWDS_CASE(16)
@@ -82,6 +82,18 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
     *handled = false;
     if (!shape_ok(B, H, L, K) || int64_t(G) * H >= (int64_t(1) << 31)) return KS_OK;
     CUtensorMap gm, xm, dm;
+    if constexpr (!DX) {
+        // rows shorter than a 2048-wide item: items of RPI whole rows of the
+        // CTA's channel ({32, L/32, H, B} view, one box per tensor per item)
+        if (L < kTT && opt(kOptDwMrow) != 0) {
+            const int npr = static_cast<int>(L / 32);
+            const int rpi = std::min(kMaxRPI, 64 / npr);
+            if (!encode_padded_view(&gm, gy, B * H, L, H, npr, 1, rpi)) return KS_OK;
+            if (!encode_padded_view(&xm, x, B * H, L, H, npr + 2, 1, rpi)) return KS_OK;
+            *handled = true;
+            return launch_any_k<kDW | kMRow>(K, true, gm, xm, gm, k, part, B, H, L, G, nullptr, st, rpi);
+        }
+    }
     if (!encode_row_view_padded(&gm, gy, B * H, L, DX ? 66 : 64)) return KS_OK;
     if (!encode_row_view_padded(&xm, x, B * H, L, kXP)) return KS_OK;
     if constexpr (DX) {

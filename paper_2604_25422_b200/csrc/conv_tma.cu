@@ -47,6 +47,27 @@ bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t 
     return r == CUDA_SUCCESS;
 }
 
+// Channel view, 128B-swizzled: the [rows, L] tensor (rows = batch x H
+// channels) as {32, L/32, H, rows/H} with box {32, n, 1, depth} -- `depth`
+// batch entries of one channel, each n 128-byte pieces (dw_tma's multi-row
+// items; the swizzle pattern follows the shared address, so the rows read
+// as one long swizzled window).
+bool encode_chan_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n, int depth) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn || L % 32 != 0 || H < 1 || rows % H != 0 || (reinterpret_cast<uintptr_t>(base) & 15) != 0) return false;
+    if (n < 1 || n > 256 || depth < 1 || depth > 256) return false;
+    if (L / 32 >= (int64_t(1) << 31) || H >= (int64_t(1) << 31) || rows / H >= (int64_t(1) << 31)) return false;
+    const cuuint64_t dims[4] = {32, static_cast<cuuint64_t>(L / 32), static_cast<cuuint64_t>(H),
+                                static_cast<cuuint64_t>(rows / H)};
+    const cuuint64_t strides[3] = {128, static_cast<cuuint64_t>(L) * 4, static_cast<cuuint64_t>(L * H) * 4};
+    const cuuint32_t box[4] = {32, static_cast<cuuint32_t>(n), 1, static_cast<cuuint32_t>(depth)};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(base), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Padded view: the [rows, L] tensor (rows = batch x H channels) as the 4-D
 // tensor {32, L/32, H, rows/H} (floats, 32-float pieces, channels, batch
 // entries) with box {36, n, chan_box, depth}.  The box's inner extent runs 4

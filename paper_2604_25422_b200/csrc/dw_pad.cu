@@ -236,10 +236,24 @@ ks_status launch(const CUtensorMap& gm, const CUtensorMap& xm, float* part, int6
 
 }  // namespace
 
-// Envelope of the compute-bound dW kernel (K >= 128, L >= 2048, L % 32 == 0).
+// Tap groups of 32 per CTA for K (the tile starts `base` <= 0 taps early so
+// the x window sits on a 32-float piece).
+static int dwpad_njg(int64_t K) {
+    const int p = static_cast<int>(K / 2);
+    const int64_t KK = K - (p % 32 ? p % 32 - 32 : 0);
+    int njg = 1;
+    while (njg < 32 && njg * kJR < KK) njg *= 2;
+    return njg;
+}
+
+// Envelope of the compute-bound dW kernel: K >= dwpad_min_k (128 by default),
+// L >= 2048, L % 32 == 0, and a row at least one work item long for the
+// tap-group count (2048 / 4096 / 8192 t at 4+ / 2 / 1 groups).
 bool dw_pad_applies(int64_t B, int64_t H, int64_t L, int64_t K) {
-    return K >= 128 && K <= 8192 && L >= 2048 && L % 32 == 0 && L < (int64_t(1) << 30) &&
-           B * H < (int64_t(1) << 31);
+    if (!(K >= std::max<int64_t>(17, opt(kOptDwpadMinK)) && K <= 8192 && L >= 2048 && L % 32 == 0 &&
+          L < (int64_t(1) << 30) && B * H < (int64_t(1) << 31)))
+        return false;
+    return L >= 32 * (kNT / dwpad_njg(K));
 }
 
 // Row groups G of dw_pad's partial buffer: enough CTAs to fill the GPU a few
@@ -257,14 +271,12 @@ int dw_pad_groups(int64_t B, int64_t H, int64_t K) {
 ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L, int64_t K,
                         int G, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
-    if (K < 128 || K > 8192 || L < 2048 || L % 32 != 0 || L >= (int64_t(1) << 30) || B * H >= (int64_t(1) << 31))
-        return KS_OK;
+    if (!dw_pad_applies(B, H, L, K)) return KS_OK;
     DwPadGeom g{};
     const int p = static_cast<int>(K / 2);
     g.base = p % 32 ? p % 32 - 32 : 0;
     const int64_t KK = K - g.base;  // taps to cover, from base
-    int njg = 4;
-    while (njg < 32 && njg * kJR < KK) njg *= 2;
+    const int njg = dwpad_njg(K);
     const int nts = kNT / njg;
     g.JT = njg * kJR;
     g.NJT = static_cast<int>((KK + g.JT - 1) / g.JT);
@@ -299,6 +311,8 @@ ks_status dw_pad_stage1(const float* gy, const float* x, float* part, int64_t B,
     (void)mode;  // HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
     *handled = true;
     switch (njg) {
+        case 1: return launch<1, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
+        case 2: return launch<2, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
         case 4: return launch<4, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
         case 8: return launch<8, true>(gm, xm, part, B, H, L, K, G, g, NS, st);
         case 16: return launch<16, true>(gm, xm, part, B, H, L, K, G, g, NS, st);

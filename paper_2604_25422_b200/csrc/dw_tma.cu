@@ -58,12 +58,20 @@ __device__ __forceinline__ int block_t(int q) {
 // swizzled output buffer, and thread 0 stores each 2048-wide tile with one
 // TMA tensor store (double-buffered).  gy and x are read from HBM once for
 // both gradients: 12 B per element instead of 16 (dX 8 + dW 8).
-template <int JR, int TB, int NJ, int S, bool FUSED, bool BWD, int S2>
+//
+// MR (dW only, L = 256 / 512 / 1024): a work item is RPI = 2048 / L whole rows
+// of the CTA's channel instead of one 2048-wide tile of one row (most of which
+// would lie past the row end): the 4-D view {32, L/32, H, B} (encode_chan_view)
+// brings RPI rows per box -- gy rows packed, so block t-offset tl addresses row
+// tl >> lsh exactly as in one long row, and each row's x window with its own
+// XT tail pieces (zero outside the row), so a row's x index moves by XT pieces
+// per row.  Same per-block math and reduction tree.
+template <int JR, int TB, int NJ, int S, bool FUSED, bool BWD, int S2, bool MR>
 __global__ void __launch_bounds__(kThreads)
 dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUtensorMap x_map,
        const __grid_constant__ CUtensorMap x_tail_map, const __grid_constant__ CUtensorMap dx_map,
        const float* __restrict__ k, float* __restrict__ part, int B, int H, int L, int K, int p, int G, int NJT,
-       DwGeomT g, int NS) {
+       DwGeomT g, int NS, int lsh, int rpi) {
     constexpr int NTS = kThreads / NJ;
     constexpr int JT = NJ * JR;
     constexpr int SPT = kDwTT / (NTS * TB);
@@ -71,6 +79,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     constexpr int NV2 = (S2 + TB + JR - 1 + 3) / 4;  // dX window quads (K <= JR)
     constexpr int GOFS = BWD ? kDwIn : 0;            // gy logical index of t0
     static_assert(!BWD || (NJ == 1 && TB == 8), "the fused backward needs one tap group of 8-wide blocks");
+    static_assert(!(BWD && MR), "multi-row items are for dW only");
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
     unsigned char* outb = smem + NS * g.stage_bytes;  // BWD: 2 x 8 KB dX tiles
@@ -89,7 +98,8 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
     const int jg = tid / NTS;
     const int ts = tid - jg * NTS;
     const int ntt = (L + kDwTT - 1) / kDwTT;
-    const int nunits = (b_end - b_begin) * ntt;
+    const int nrows = b_end - b_begin;
+    const int nunits = MR ? (nrows + rpi - 1) / rpi : nrows * ntt;
     // the x window of a work item at t0 starts at position t0 + j0 - p - D
     const int xoff = j0 - p;
     const int D = ((xoff % kDwIn) + kDwIn) % kDwIn;
@@ -108,6 +118,14 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
 
     const uint32_t tx_bytes = static_cast<uint32_t>(g.gy_box * kDwIn * 4 + g.XR * kDwIn * 4);
     auto issue = [&](int stage, int u) {
+        if constexpr (MR) {  // rows b .. b + rpi - 1 of channel h: gy packed, x windows with their tails
+            const int b = b_begin + u * rpi;
+            unsigned char* sb = smem + stage * g.stage_bytes;
+            mbar_arrive_expect_tx(&full[stage], tx_bytes);
+            tma_load_pad(sb, &gy_map, 0, h, b, &full[stage]);
+            tma_load_pad(sb + g.gy_bytes, &x_map, xr_rel, h, b, &full[stage]);
+            return;
+        }
         const int b = b_begin + u / ntt;
         const int t0 = (u % ntt) * kDwTT;
         const int row = b * H + h;
@@ -141,11 +159,12 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
         const unsigned char* gys = smem + stage * g.stage_bytes;
         const unsigned char* xs = gys + g.gy_bytes;
         unsigned char* ob = outb + (u & 1) * kDwTT * 4;
-        const int t0 = (u % ntt) * kDwTT;
+        const int t0 = MR ? 0 : (u % ntt) * kDwTT;
+        const int tlim = MR ? min(rpi, nrows - u * rpi) << lsh : L - t0;  // live blocks: tl < tlim
 #pragma unroll 2
         for (int s = 0; s < SPT; ++s) {
             const int tl = block_t<TB>(s * NTS + ts);
-            if (t0 + tl < L) {
+            if (tl < tlim) {
                 float gv[TB];
 #pragma unroll
                 for (int c = 0; c < TB / 4; ++c) {
@@ -157,7 +176,7 @@ dw_tma(const __grid_constant__ CUtensorMap gy_map, const __grid_constant__ CUten
                     gv[4 * c + 3] = q.w;
                 }
                 float xv[4 * NVX];
-                const uint32_t xi = static_cast<uint32_t>(A + tl + jg * JR);
+                const uint32_t xi = static_cast<uint32_t>(A + tl + jg * JR + (MR ? (tl >> lsh) * g.XT * kDwIn : 0));
 #pragma unroll
                 for (int c = 0; c < NVX; ++c) {
                     const float4 q = lds4(xs + swz<128>(xi + 4 * c));
@@ -244,18 +263,25 @@ struct Maps {
 
 template <int JR, int TB, int NJ, bool FUSED, bool BWD>
 ks_status launch(int s, int s2, const Maps& mp, const float* k, float* part, int64_t B, int64_t H, int64_t L,
-                 int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
+                 int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st, int lsh = -1, int rpi = 0) {
     const int smem = NS * g.stage_bytes + (BWD ? 2 * kDwTT * 4 : 0) + 64 + 1024;
     const unsigned blocks = static_cast<unsigned>(int64_t(G) * H * NJT);
     const int p = static_cast<int>(K / 2);
-#define KS_DW_CASE(SV, S2V)                                                                                    \
+#define KS_DW_CASE_M(SV, S2V, MRV)                                                                             \
     if (s == SV && s2 == S2V) {                                                                                \
-        auto kern = dw_tma<JR, TB, NJ, SV, FUSED, BWD, S2V>;                                                   \
+        auto kern = dw_tma<JR, TB, NJ, SV, FUSED, BWD, S2V, MRV>;                                              \
         prepare_kernel(reinterpret_cast<const void*>(kern), kThreads, smem);                                 \
         launch_kernel(kern, blocks, kThreads, smem, st, mp.gm, mp.xm, mp.xt, mp.dxm, k, part, static_cast<int>(B),        \
                                              static_cast<int>(H), static_cast<int>(L), static_cast<int>(K), p, \
-                                             G, NJT, g, NS);                                                   \
+                                             G, NJT, g, NS, lsh, rpi);                                         \
         return check_launch();                                                                                 \
+    }
+#define KS_DW_CASE(SV, S2V) KS_DW_CASE_M(SV, S2V, false)
+    if constexpr (!BWD) {
+        if (rpi > 0) {
+            KS_DW_CASE_M(0, 0, true) KS_DW_CASE_M(1, 0, true) KS_DW_CASE_M(2, 0, true) KS_DW_CASE_M(3, 0, true)
+            return KS_ERR_CUDA;
+        }
     }
     if constexpr (BWD) {
         // S2 = (-q) mod 4 with q = K-1-p: S2 = S for odd K, S + 1 (mod 4) for even K
@@ -265,14 +291,16 @@ ks_status launch(int s, int s2, const Maps& mp, const float* k, float* part, int
         KS_DW_CASE(0, 0) KS_DW_CASE(1, 0) KS_DW_CASE(2, 0) KS_DW_CASE(3, 0)
     }
 #undef KS_DW_CASE
+#undef KS_DW_CASE_M
     return KS_ERR_CUDA;
 }
 
 template <int JR, int TB, int NJ, bool BWD>
 ks_status launch_m(int s, int s2, bool fused, const Maps& mp, const float* k, float* part, int64_t B, int64_t H,
-                   int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st) {
-    return fused ? launch<JR, TB, NJ, true, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st)
-                 : launch<JR, TB, NJ, false, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st);
+                   int64_t L, int64_t K, int G, int NJT, const DwGeomT& g, int NS, cudaStream_t st, int lsh = -1,
+                   int rpi = 0) {
+    return fused ? launch<JR, TB, NJ, true, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st, lsh, rpi)
+                 : launch<JR, TB, NJ, false, BWD>(s, s2, mp, k, part, B, H, L, K, G, NJT, g, NS, st, lsh, rpi);
 }
 
 // Shared by the dW-only and the fused backward entry points.
@@ -297,16 +325,30 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
     g.gy_bytes = (g.gy_box * kDwIn * 4 + 1023) / 1024 * 1024;
     g.XT = (nj * JR + 40 + kDwIn - 1) / kDwIn;  // covers D + JT + the register-window overrun
     g.XR = kDwMain + g.XT;
-    g.stage_bytes = (g.gy_bytes + g.XR * kDwIn * 4 + 1023) / 1024 * 1024;
     Maps mp;
-    if (!encode_row_view(&mp.gm, gy, B * H, L, kDwIn, g.gy_box, 128)) return KS_OK;
-    if (!encode_row_view(&mp.xm, x, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
-    if (!encode_row_view(&mp.xt, x, B * H, L, kDwIn, g.XT, 128)) return KS_OK;
-    if (bwd) {
-        if (!encode_row_view(&mp.dxm, dx, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
-    } else {
+    // rows of 256 / 512 / 1024: items of 2048 / L whole rows (see the kernel)
+    int lsh = -1, rpi = 0;
+    if (!bwd && L < kDwTT && L >= 256 && (L & (L - 1)) == 0 && opt(kOptDwMrow) != 0) {
+        const int npr = static_cast<int>(L / kDwIn);
+        rpi = static_cast<int>(kDwTT / L);
+        lsh = 0;
+        while ((int64_t(1) << lsh) < L) ++lsh;
+        g.XR = rpi * (npr + g.XT);
+        if (!encode_chan_view(&mp.gm, gy, B * H, L, H, npr, rpi)) return KS_OK;
+        if (!encode_chan_view(&mp.xm, x, B * H, L, H, npr + g.XT, rpi)) return KS_OK;
+        mp.xt = mp.xm;   // unused
         mp.dxm = mp.gm;  // unused
+    } else {
+        if (!encode_row_view(&mp.gm, gy, B * H, L, kDwIn, g.gy_box, 128)) return KS_OK;
+        if (!encode_row_view(&mp.xm, x, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+        if (!encode_row_view(&mp.xt, x, B * H, L, kDwIn, g.XT, 128)) return KS_OK;
+        if (bwd) {
+            if (!encode_row_view(&mp.dxm, dx, B * H, L, kDwIn, kDwMain, 128)) return KS_OK;
+        } else {
+            mp.dxm = mp.gm;  // unused
+        }
     }
+    g.stage_bytes = (g.gy_bytes + g.XR * kDwIn * 4 + 1023) / 1024 * 1024;
     // 4 stages for the lightest blocks (K <= 8: bandwidth wants bytes in flight);
     // 3 for K > 8, where a fourth CTA per SM hides more FMA latency
     // (config 5a dW 10.7 -> 10.1 ms, fused backward 22.4 -> 20.4 ms)
@@ -322,14 +364,14 @@ ks_status run_dw_tma(const float* gy, const float* x, const float* k, float* dx,
         return j16 ? launch_m<16, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st)
                    : launch_m<8, 8, 1, true>(s, s2, fused, mp, k, part, B, H, L, K, G, njt, g, NS, st);
     // dW only: HIERARCHICAL accumulates with FMA in either MulAddMode (conv_dw.cu)
-    if (j16) return launch<16, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+    if (j16) return launch<16, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi);
     if (JR == 8)
-        return nj == 1 ? launch<8, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st)
-                       : launch<8, 8, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        return nj == 1 ? launch<8, 8, 1, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi)
+                       : launch<8, 8, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi);
     switch (nj) {
-        case 2: return launch<16, 16, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
-        case 4: return launch<16, 16, 4, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
-        default: return launch<16, 16, 8, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st);
+        case 2: return launch<16, 16, 2, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi);
+        case 4: return launch<16, 16, 4, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi);
+        default: return launch<16, 16, 8, true, false>(s, 0, mp, k, part, B, H, L, K, G, njt, g, NS, st, lsh, rpi);
     }
 }
 

@@ -107,6 +107,8 @@ enum Opt {
     kOptHostBlockMb,
     kOptStencilBl,
     kOptDwCtas,
+    kOptDwMrow,
+    kOptDwpadMinK,
     kOptStsRows,
     kOptCount
 };

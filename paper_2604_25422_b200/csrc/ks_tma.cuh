@@ -233,6 +233,7 @@ bool encode_row_view(CUtensorMap* map, const float* base, int64_t rows, int64_t 
 // (rows = batch x H channels) with box {36, n, chan_box, depth}: every
 // 32-float piece lands as a 36-float shared row (conflict-free 128-bit reads
 // 144 B apart, no re-layout pass).
+bool encode_chan_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n, int depth);
 bool encode_padded_view(CUtensorMap* map, const float* base, int64_t rows, int64_t L, int64_t H, int n,
                         int chan_box, int depth);
 

@@ -27,7 +27,7 @@ struct OptDef {
 // order = enum Opt (ks_common.cuh)
 constexpr OptDef kDefs[kOptCount] = {
     {"disable_tma", 0, 0, 1},    // 1: generic (non-TMA) kernels only
-    {"ldg", 1, 0, 2},            // stencil_ldg for fwd/dX: 0 never, 1 K <= 10, 2 K <= 16
+    {"ldg", 1, 0, 2},            // stencil_ldg for fwd/dX (L >= 256): 0 never, 1 auto (K <= 10; L < 2048: K <= 12, Fused K <= 16 from L = 1024), 2 K <= 16
     {"sts", 1, 0, 1},            // K <= 16 fwd/dX through bwd_short (0: stencil_tma)
     {"bwds", 1, 0, 1},           // K <= 16 dW / fused backward through bwd_short (0: dw_tma)
     {"dst", 0, 0, 1},            // bwd_short stencil outputs by 256-bit stores instead of TMA stores
@@ -44,6 +44,8 @@ constexpr OptDef kDefs[kOptCount] = {
     {"host_block_mb", 64, 1, 4096},  // host-buffer entry points: bytes per streamed block
     {"stencil_bl", -1, -1, 1},   // stencil_pad's batch-lane kernel: 1 always, 0 never, -1 auto (K >= L / 4)
     {"dw_ctas", 8192, 64, 1 << 20},
+    {"dw_mrow", 1, 0, 1},
+    {"dwpad_min_k", 128, 17, 8192},  // smallest K whose dW takes dw_pad (below: dw_tma)        // K <= 16 dW with L < 2048: items of whole rows (0: one 2048-wide tile per row)
     {"sts_rows", -1, -1, 1},     // bwd_short stencils: one CTA per row (1), persistent grid (0), -1 auto (rows in Fused mode)  // HIERARCHICAL stage 1 (dw_tma / bwd_short / dw_rows / generic): target CTAs (sets G)
 };
 

@@ -38,7 +38,10 @@ __device__ __forceinline__ void st_v8(float* p, const float (&d)[8]) {
 
 // REV = 0: forward (off = p = K/2); REV = 1: dX (off = q = K-1-p).  kp: the
 // prepared taps [H, 16] (reversed for dX, zero past K).
-template <int KT, bool FUSED, bool REV>
+// V8: L % 8 == 0 and a 32-byte aligned output -- one 256-bit store per
+// thread; otherwise (L % 8 == 4) two 128-bit stores, the second dropped for
+// the last half-block of a row.
+template <int KT, bool FUSED, bool REV, bool V8>
 __global__ void __launch_bounds__(256)
 stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* __restrict__ out, int tpr, int H,
             int L) {
@@ -66,7 +69,7 @@ stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* 
 #pragma unroll
     for (int c = 0; c < NV; ++c) {
         const int s = a0 + 4 * c;
-        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);   // quads are wholly in or out of the row (L % 8 == 0)
+        float4 q = make_float4(0.f, 0.f, 0.f, 0.f);   // quads are wholly in or out of the row (L % 4 == 0)
         if (s >= 0 && s < L) q = *reinterpret_cast<const float4*>(xr + s);
         v[4 * c + 0] = q.x;
         v[4 * c + 1] = q.y;
@@ -80,7 +83,13 @@ stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* 
     for (int jj = 0; jj < KT; ++jj)
 #pragma unroll
         for (int r = 0; r < 8; ++r) d[r] = muladd<FUSED>(d[r], v[S + r + jj], w[jj]);
-    st_v8(out + static_cast<int64_t>(row) * L + t, d);
+    float* o = out + static_cast<int64_t>(row) * L + t;
+    if constexpr (V8) {
+        st_v8(o, d);
+    } else {
+        *reinterpret_cast<float4*>(o) = make_float4(d[0], d[1], d[2], d[3]);
+        if (t + 8 <= L) *reinterpret_cast<float4*>(o + 4) = make_float4(d[4], d[5], d[6], d[7]);
+    }
 }
 
 template <int KT, bool REV>
@@ -89,8 +98,14 @@ ks_status launch_k(bool fused, const float* in, const float4* kp, float* out, in
     const int tpr = static_cast<int>((L + 2047) / 2048);
     const unsigned grid = static_cast<unsigned>(rows * tpr);
     const int h = static_cast<int>(H), l = static_cast<int>(L);
-    if (fused) launch_kernel(stencil_ldg<KT, true, REV>, grid, 256, 0, st, in, kp, out, tpr, h, l);
-    else launch_kernel(stencil_ldg<KT, false, REV>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+    const bool v8 = L % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
+    if (v8) {
+        if (fused) launch_kernel(stencil_ldg<KT, true, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+        else launch_kernel(stencil_ldg<KT, false, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+    } else {
+        if (fused) launch_kernel(stencil_ldg<KT, true, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+        else launch_kernel(stencil_ldg<KT, false, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+    }
     return check_launch();
 }
 
@@ -111,8 +126,9 @@ ks_status launch_any(int64_t K, bool fused, const float* in, const float4* kp, f
 }  // namespace
 
 // *handled = false when the shape / alignment is outside this kernel's
-// envelope (L % 8 == 0, 16-byte input and 32-byte output bases) or the knob
-// says otherwise.  Default: K <= 10 (round-2 ABAB
+// envelope (L % 4 == 0, 16-byte aligned bases; 256-bit stores where L % 8 == 0
+// and the output is 32-byte aligned) or the knob
+// says otherwise.  Default on rows of 2048 or more: K <= 10 (round-2 ABAB
 // sweep over K = 9..16 at (256,512,8192,K), tools/sweep_options.py,
 // gpurun_out/s5: K = 9 fwd 1.45 -> 1.25 ms Fused, 1.50 -> 1.32 Separate;
 // K = 10 Fused 1.46 -> 1.36, Separate even; K >= 11 the TMA kernels win,
@@ -126,10 +142,18 @@ ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B
                           int64_t off, int reverse, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
     const int knob = static_cast<int>(opt(kOptLdg));
-    if (knob == 0 || K > (knob >= 2 ? 16 : 10)) return KS_OK;
-    if (K < 1 || K > 16 || L % 8 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
+    if (knob == 0 || L < 256) return KS_OK;
+    // default (knob 1): K <= 10 on long rows; below L = 2048 -- where the TMA
+    // kernels' 2048-wide items run partly past the row end -- K <= 12, and
+    // K <= 16 in Fused mode from L = 1024 (round-2 ABAB over L = 256..1984,
+    // gpurun_out/s18: K <= 12 -7..-36%, K = 16 Fused at L = 1984 -31%,
+    // K = 16 Separate or L = 256 slower)
+    const bool fused_mode = mode == KS_MULADD_FUSED;
+    const int64_t kmax = knob >= 2 ? 16 : L >= 2048 ? 10 : (fused_mode && L >= 1024) ? 16 : 12;
+    if (K > kmax) return KS_OK;
+    if (K < 1 || K > 16 || L % 4 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;
-    if ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 31) != 0) return KS_OK;
+    if ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
     const int64_t rows = B * H;
     if (rows * ((L + 2047) / 2048) >= (int64_t(1) << 31)) return KS_OK;
     float* kp = nullptr;

@@ -73,6 +73,8 @@ def logical_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
 def _stencil_tier(L: int, K: int, B: int = 1):
     if L < 1024 and L % 4 == 0 and L + K - 1 <= 252:
         return "stencil_rows", 16, None
+    if L % 4 == 0 and L >= 256 and (K <= 10 or (L < 2048 and K <= 12)):  # Separate mode's rule (stencil_ldg_f32)
+        return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if L % 32 != 0 or K > 8192:
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
     if K > 32 and L >= 1024 and B >= 32 and 4 * K >= L:
@@ -82,8 +84,6 @@ def _stencil_tier(L: int, K: int, B: int = 1):
     # Separate mode (the reference's default, which this model and the committed
     # plans follow) below K = 1024: stencil_tma's register tiles (Fused mode
     # takes stencil_pad here too)
-    if K <= 10 and L >= 1024:
-        return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if K <= 16 and L >= 1024:
         return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
     if K > 32 and L >= 2048:  # stencil_tma.cu pick_tile
@@ -225,8 +225,11 @@ def _bwd_short(mode: str, B, H, L, K, G, occ):
     gy_region = _cdiv(gyp * 144, 128) * 128
     x_region = _cdiv(66 * 144, 128) * 128
     has_dw, has_st = mode in ("dw", "fused"), mode in ("fused", "fwd", "dx")
+    mrow = mode == "dw" and L < 2048  # items of whole rows: each row's x window has its own 2 halo pieces
+    if mrow:
+        x_region = _cdiv((64 + 2 * 8) * 144, 128) * 128
     stage = gy_region + (x_region if has_dw else 0) + (128 if mode in ("fwd", "dx") else 0)
-    ns = 4 if mode in ("fwd", "dx") else (4 if K <= 8 else 3)
+    ns = 4 if mode in ("fwd", "dx") else 3 if mrow else (4 if K <= 8 else 3)
     smem = (2 * 8192 if has_st else 0) + ns * stage + 64 + 1024
     # stencils: persistent in Separate mode (the plans and this model are for
     # Separate, the reference's default); Fused mode launches one CTA per row
@@ -352,7 +355,10 @@ def _dw_tma(B, H, L, K, G):
     njt = _cdiv(K, nj * jr)
     gy_bytes = _cdiv(64 * 32 * 4, 1024) * 1024
     xt = _cdiv(nj * jr + 40, 32)
-    stage = _cdiv(gy_bytes + (64 + xt) * 128, 1024) * 1024
+    xr = 64 + xt
+    if 256 <= L < 2048 and L & (L - 1) == 0:  # multi-row items: 2048 / L rows, each x window with its own tail
+        xr = (2048 // L) * (L // 32 + xt)
+    stage = _cdiv(gy_bytes + xr * 128, 1024) * 1024
     ns = max(2, min(3 if K > 8 else 4, 72 * 1024 // stage))
     return _launch("dw_tma", G * H * njt, 256, ns * stage + 64 + 1024)
 

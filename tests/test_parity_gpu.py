@@ -418,12 +418,15 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
 
 
 @pytest.mark.parametrize("shape", [(24, 8, 256, 32), (12, 8, 512, 300), (10, 6, 768, 40), (16, 4, 128, 200),
-                                   (8, 4, 992, 1000), (6, 5, 64, 500)])
+                                   (8, 4, 992, 1000), (6, 5, 64, 500), (40, 6, 256, 7), (20, 4, 512, 12),
+                                   (12, 3, 1024, 16), (9, 2, 1984, 13), (30, 3, 256, 16), (7, 5, 500, 7),
+                                   (5, 3, 1000, 12), (3, 7, 4092, 5), (4, 3, 2052, 9)])
 def test_mid_length_rows_register_tiles(oracle, shape):
-    """Rows shorter than 1024 whose L + K is too long for the whole-row
-    kernels (stencil_rows): stencil_tma's R = 4 tiles sized to the row
-    (32..256 threads), y and dX bitwise against the oracle in both modes,
-    every channel."""
+    """Rows shorter than 2048 that the whole-row kernels (stencil_rows) do
+    not take: stencil_tma's R = 4 tiles sized to the row (32..256 threads),
+    stencil_ldg's register windows (K <= 12, or K <= 16 in Fused mode from
+    L = 1024) and bwd_short (K = 13..16 in Separate mode from L = 1024) --
+    y and dX bitwise against the oracle in both modes, every channel."""
     B, H, L, K = shape
     x, k, gy = ks.make_inputs(21, B, H, L, K)
     xh, gh, kh = host(x), host(gy), host(k)
@@ -431,6 +434,51 @@ def test_mid_length_rows_register_tiles(oracle, shape):
         y, dx = host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))
         assert same(y, oracle.forward(xh, kh, m)), m
         assert same(dx, oracle.backward_input(gh, kh, m)), m
+
+
+@pytest.mark.parametrize("shape", [(37, 6, 256, 7), (21, 5, 512, 16), (9, 4, 768, 1), (13, 3, 1024, 12),
+                                   (11, 2, 1056, 9), (7, 3, 1984, 16), (300, 4, 256, 3), (37, 6, 256, 40),
+                                   (21, 5, 512, 64), (13, 3, 1024, 100), (19, 2, 256, 17), (9, 3, 768, 24)])
+def test_dw_multirow_items(oracle, shape):
+    """dW on rows shorter than one 2048-wide item: items of RPI whole rows of
+    a channel (bwd_short MODE dW | kMRow for K <= 16, dw_tma MR for K > 16 at
+    L = 256 / 512 / 1024), ragged last items (B not a multiple of RPI, several
+    row groups), each row's own zero halo: dk within
+    the HIERARCHICAL tolerance of fp64 on every channel, run-to-run bitwise,
+    and the single-row item path (option dw_mrow = 0) within tolerance too."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(17, B, H, L, K)
+    dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+    assert same(dk, host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, SEPARATE)))
+    with ks.options(dw_mrow=0):
+        dk1 = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+    xh, gh = host(x), host(gy)
+    for h in range(H):
+        xs, gs = np.ascontiguousarray(xh[:, h:h + 1]), np.ascontiguousarray(gh[:, h:h + 1])
+        truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+        assert normwise(dk[h:h + 1], truth) <= HIER_TOL, h
+        assert normwise(dk1[h:h + 1], truth) <= HIER_TOL, h
+
+
+@pytest.mark.parametrize("shape", [(4, 8, 8192, 24), (6, 4, 4096, 48), (3, 4, 16384, 64), (5, 3, 4096, 100),
+                                   (2, 3, 8192, 33)])
+def test_dw_pad_below_128_taps(oracle, shape):
+    """dw_pad with one or two 32-tap groups per CTA (option dwpad_min_k
+    lowers its K threshold; rows at least one work item long): dk within the
+    HIERARCHICAL tolerance of fp64 on every channel, run-to-run bitwise, as is
+    the default tier's."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(19, B, H, L, K)
+    with ks.options(dwpad_min_k=17):
+        dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+        assert same(dk, host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED)))
+    dk0 = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+    xh, gh = host(x), host(gy)
+    for h in range(H):
+        xs, gs = np.ascontiguousarray(xh[:, h:h + 1]), np.ascontiguousarray(gh[:, h:h + 1])
+        truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+        assert normwise(dk[h:h + 1], truth) <= HIER_TOL, h
+        assert normwise(dk0[h:h + 1], truth) <= HIER_TOL, h
 
 
 @pytest.mark.parametrize("K", [1, 4, 7, 10, 13, 16])
