@@ -246,7 +246,9 @@ static int dwpad_njg(int64_t K) {
     return njg;
 }
 
-// Envelope of the compute-bound dW kernel: K >= dwpad_min_k (128 by default),
+// Envelope of the compute-bound dW kernel: K >= dwpad_min_k (48 by default:
+// round-2 ABAB against dw_tma, gpurun_out/s21 -- K = 48 / 64 / 100 at
+// L >= 4096: -21 / -14 / -29%; K = 24 / 32: +29-40%, so they stay on dw_tma),
 // L >= 2048, L % 32 == 0, and a row at least one work item long for the
 // tap-group count (2048 / 4096 / 8192 t at 4+ / 2 / 1 groups).
 bool dw_pad_applies(int64_t B, int64_t H, int64_t L, int64_t K) {

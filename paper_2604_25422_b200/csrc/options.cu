@@ -45,7 +45,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"stencil_bl", -1, -1, 1},   // stencil_pad's batch-lane kernel: 1 always, 0 never, -1 auto (K >= L / 4)
     {"dw_ctas", 8192, 64, 1 << 20},
     {"dw_mrow", 1, 0, 1},
-    {"dwpad_min_k", 128, 17, 8192},  // smallest K whose dW takes dw_pad (below: dw_tma)        // K <= 16 dW with L < 2048: items of whole rows (0: one 2048-wide tile per row)
+    {"dwpad_min_k", 48, 17, 8192},   // smallest K whose dW takes dw_pad (below: dw_tma)        // K <= 16 dW with L < 2048: items of whole rows (0: one 2048-wide tile per row)
     {"sts_rows", -1, -1, 1},     // bwd_short stencils: one CTA per row (1), persistent grid (0), -1 auto (rows in Fused mode)  // HIERARCHICAL stage 1 (dw_tma / bwd_short / dw_rows / generic): target CTAs (sets G)
 };
 

@@ -44,14 +44,24 @@ __device__ __forceinline__ void st_v8(float* p, const float (&d)[8]) {
 template <int KT, bool FUSED, bool REV, bool V8>
 __global__ void __launch_bounds__(256)
 stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* __restrict__ out, int tpr, int H,
-            int L) {
+            int L, int rows, int rpc, int tprow) {
     constexpr int OFF = REV ? KT - 1 - KT / 2 : KT / 2;
     constexpr int S = (4 - OFF % 4) % 4;              // window starts S floats into its first quad
     constexpr int NV = (S + 8 + KT - 1 + 3) / 4;      // quads per window
     // CTA = (row, 2048-output tile): the row, channel and tile are CTA-uniform
-    // (uniform datapath), the thread's 8 outputs start at 8 * threadIdx.x
-    const int row = static_cast<int>(blockIdx.x) / tpr;
-    const int t = (static_cast<int>(blockIdx.x) - row * tpr) * 2048 + 8 * static_cast<int>(threadIdx.x);
+    // (uniform datapath), the thread's 8 outputs start at 8 * threadIdx.x.
+    // Rows shorter than 1024 (rpc > 1): a CTA takes rpc whole rows, tprow =
+    // ceil(L / 8) threads each, instead of leaving most of its threads idle.
+    int row, t;
+    if (rpc > 1) {
+        const int r = static_cast<int>(threadIdx.x) / tprow;
+        row = static_cast<int>(blockIdx.x) * rpc + r;
+        t = 8 * (static_cast<int>(threadIdx.x) - r * tprow);
+        if (r >= rpc || row >= rows) return;
+    } else {
+        row = static_cast<int>(blockIdx.x) / tpr;
+        t = (static_cast<int>(blockIdx.x) - row * tpr) * 2048 + 8 * static_cast<int>(threadIdx.x);
+    }
     if (t >= L) return;
     const int h = row % H;
     float w[16];
@@ -96,15 +106,17 @@ template <int KT, bool REV>
 ks_status launch_k(bool fused, const float* in, const float4* kp, float* out, int64_t rows, int64_t H, int64_t L,
                    cudaStream_t st) {
     const int tpr = static_cast<int>((L + 2047) / 2048);
-    const unsigned grid = static_cast<unsigned>(rows * tpr);
-    const int h = static_cast<int>(H), l = static_cast<int>(L);
+    const int tprow = static_cast<int>((L + 7) / 8);
+    const int rpc = L < 1024 ? 256 / tprow : 1;
+    const unsigned grid = static_cast<unsigned>(rpc > 1 ? (rows + rpc - 1) / rpc : rows * tpr);
+    const int h = static_cast<int>(H), l = static_cast<int>(L), nr = static_cast<int>(rows);
     const bool v8 = L % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
     if (v8) {
-        if (fused) launch_kernel(stencil_ldg<KT, true, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l);
-        else launch_kernel(stencil_ldg<KT, false, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+        if (fused) launch_kernel(stencil_ldg<KT, true, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
+        else launch_kernel(stencil_ldg<KT, false, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
     } else {
-        if (fused) launch_kernel(stencil_ldg<KT, true, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l);
-        else launch_kernel(stencil_ldg<KT, false, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l);
+        if (fused) launch_kernel(stencil_ldg<KT, true, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
+        else launch_kernel(stencil_ldg<KT, false, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
     }
     return check_launch();
 }
@@ -149,7 +161,8 @@ ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B
     // gpurun_out/s18: K <= 12 -7..-36%, K = 16 Fused at L = 1984 -31%,
     // K = 16 Separate or L = 256 slower)
     const bool fused_mode = mode == KS_MULADD_FUSED;
-    const int64_t kmax = knob >= 2 ? 16 : L >= 2048 ? 10 : (fused_mode && L >= 1024) ? 16 : 12;
+    // rows the TMA views cannot take (L % 32 != 0) have no better kernel up to K = 16
+    const int64_t kmax = knob >= 2 || L % 32 != 0 ? 16 : L >= 2048 ? 10 : (fused_mode && L >= 1024) ? 16 : 12;
     if (K > kmax) return KS_OK;
     if (K < 1 || K > 16 || L % 4 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;

@@ -73,7 +73,8 @@ def logical_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
 def _stencil_tier(L: int, K: int, B: int = 1):
     if L < 1024 and L % 4 == 0 and L + K - 1 <= 252:
         return "stencil_rows", 16, None
-    if L % 4 == 0 and L >= 256 and (K <= 10 or (L < 2048 and K <= 12)):  # Separate mode's rule (stencil_ldg_f32)
+    if L % 4 == 0 and L >= 256 and (K <= 10 or (L < 2048 and K <= 12) or (L % 32 != 0 and K <= 16)):
+        # Separate mode's rule (stencil_ldg_f32)
         return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if L % 32 != 0 or K > 8192:
         return "conv_tile_f32", 16 if L > 1024 else 4, 256
@@ -94,8 +95,18 @@ def _stencil_tier(L: int, K: int, B: int = 1):
     return "stencil_tma", 4, 256 if L > 512 else 128 if L > 256 else 64 if L > 128 else 32
 
 
+def _dwpad_njg(K: int) -> int:
+    p = K // 2
+    kk = K - (p % 32 - 32 if p % 32 else 0)
+    njg = 1
+    while njg < 32 and njg * 32 < kk:
+        njg *= 2
+    return njg
+
+
 def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
-    if K >= 128 and L >= 2048 and L % 32 == 0:
+    # dw_pad.cu dw_pad_applies: K >= 48 (option dwpad_min_k), a row at least one work item long
+    if K >= 48 and L >= 2048 and L % 32 == 0 and L >= 32 * (256 // _dwpad_njg(K)):
         njg = 4
         while njg < 32 and njg * 32 < K:
             njg *= 2
@@ -327,9 +338,7 @@ def _dw_pad(B, H, L, K, G):
     p = K // 2
     base = p % 32 - 32 if p % 32 else 0
     kk = K - base
-    njg = 4
-    while njg < 32 and njg * 32 < kk:
-        njg *= 2
+    njg = _dwpad_njg(K)
     nts = 256 // njg
     jt = njg * 32
     njt = _cdiv(kk, jt)
@@ -407,8 +416,10 @@ def launch_geometry(path: str, B: int, H: int, L: int, K: int, scheme: str = "hi
     if path in ("fwd", "dx"):
         off = K // 2 if path == "fwd" else K - 1 - K // 2
         kind = pl["kernel"]
-        if kind == "stencil_ldg":
-            return [_prep_taps(H, 16), _launch("stencil_ldg", B * H * _cdiv(L, 2048), 256, 0)]
+        if kind == "stencil_ldg":  # rows shorter than 1024: 256 // ceil(L/8) rows per CTA
+            rpc = 256 // _cdiv(L, 8) if L < 1024 else 1
+            grid = _cdiv(B * H, rpc) if rpc > 1 else B * H * _cdiv(L, 2048)
+            return [_prep_taps(H, 16), _launch("stencil_ldg", grid, 256, 0)]
         if kind == "stencil_short":
             return [_prep_taps(H, 16), _bwd_short(path, B, H, L, K, 1, occ)]
         if kind == "stencil_pad":

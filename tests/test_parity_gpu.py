@@ -420,7 +420,8 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
 @pytest.mark.parametrize("shape", [(24, 8, 256, 32), (12, 8, 512, 300), (10, 6, 768, 40), (16, 4, 128, 200),
                                    (8, 4, 992, 1000), (6, 5, 64, 500), (40, 6, 256, 7), (20, 4, 512, 12),
                                    (12, 3, 1024, 16), (9, 2, 1984, 13), (30, 3, 256, 16), (7, 5, 500, 7),
-                                   (5, 3, 1000, 12), (3, 7, 4092, 5), (4, 3, 2052, 9)])
+                                   (5, 3, 1000, 12), (3, 7, 4092, 5), (4, 3, 2052, 9), (5, 3, 1000, 16),
+                                   (7, 5, 500, 14), (33, 3, 260, 5)])
 def test_mid_length_rows_register_tiles(oracle, shape):
     """Rows shorter than 2048 that the whole-row kernels (stencil_rows) do
     not take: stencil_tma's R = 4 tiles sized to the row (32..256 threads),
