@@ -44,11 +44,12 @@ struct DwGeom {
     static constexpr int SPT = kDwTT / (NTS * kTB);  // register blocks per tile per thread
     static constexpr int NVX = (S + kTB + kJR - 1 + 3) / 4;
     static constexpr int XL = kDwTT + JT + 8;  // staged x window (logical floats, %4 == 0)
+    static constexpr int MAXR = 8;             // rows per item on rows shorter than the tile
     static constexpr int GY_FLOATS = padded_len(kDwTT);
-    static constexpr int X_FLOATS = padded_len(XL);
+    static constexpr int X_FLOATS = padded_len(XL + (MAXR - 1) * (JT + 8));
 };
 
-template <int NJ, int S, bool FUSED>
+template <int NJ, int S, bool FUSED, bool MR>
 __global__ void __launch_bounds__(kDwThreads)
 dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
                float* __restrict__ part, int B, int H, int L, int K, int p, int G, int NJT) {
@@ -75,29 +76,47 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
 #pragma unroll
     for (int i = 0; i < kJR; ++i) acc[i] = 0.f;
 
-    for (int b = b_begin; b < b_end; ++b) {
-        const int64_t row = static_cast<int64_t>(b) * H + h;
-        const float* rg = gy + row * L;
-        const float* rx = x + row * L;
+    // rows shorter than the 2048-wide tile: an item is R whole rows, row r at
+    // tile offset r * Lp (Lp = L rounded up to a t block; gy zero in between)
+    // with its own x window (XW = Lp + JT + 8 floats, its own zero halo), so
+    // a block's x index moves by XW - Lp per row
+    const int Lp = (L + kTB - 1) / kTB * kTB;
+    const int R = MR ? min(Geo::MAXR, kDwTT / Lp) : 1;  // MR: the host picks it for L <= 512
+    const int XW = Lp + Geo::JT + 8;
+    for (int b = b_begin; b < b_end; b += R) {
+        const int nr = min(R, b_end - b);
         for (int t0 = 0; t0 < L; t0 += kDwTT) {
             // stage gy tile
             for (int c = tid; c < kDwTT / 4; c += kDwThreads) {
-                const int q = t0 + 4 * c;
-                float4 v;
-                if (vec_ok && q + 3 < L) {
-                    v = ld_nc_v4(rg + q);
-                } else {
-                    v.x = q + 0 < L ? rg[q + 0] : 0.f;
-                    v.y = q + 1 < L ? rg[q + 1] : 0.f;
-                    v.z = q + 2 < L ? rg[q + 2] : 0.f;
-                    v.w = q + 3 < L ? rg[q + 3] : 0.f;
+                int q = t0 + 4 * c, r = 0;
+                if (MR) {
+                    r = (4 * c) / Lp;
+                    q = 4 * c - r * Lp;
+                }
+                float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (r < nr) {
+                    const float* rg = gy + (static_cast<int64_t>(b + r) * H + h) * L;
+                    if (vec_ok && q + 3 < L) {
+                        v = ld_nc_v4(rg + q);
+                    } else {
+                        v.x = q + 0 < L ? rg[q + 0] : 0.f;
+                        v.y = q + 1 < L ? rg[q + 1] : 0.f;
+                        v.z = q + 2 < L ? rg[q + 2] : 0.f;
+                        v.w = q + 3 < L ? rg[q + 3] : 0.f;
+                    }
                 }
                 *reinterpret_cast<float4*>(gys + pad_idx(4 * c)) = v;
             }
-            // stage x window, logical index i <-> x position a0 + i
+            // stage x window(s), logical index i <-> x position a0 + i (of row r's window)
             const int a0 = t0 + j0 - p - S;
-            for (int c = tid; c < Geo::XL / 4; c += kDwThreads) {
-                const int q = a0 + 4 * c;
+            const int nxw = MR ? nr * XW : Geo::XL;
+            for (int c = tid; c < nxw / 4; c += kDwThreads) {
+                int q = a0 + 4 * c, r = 0;
+                if (MR) {
+                    r = (4 * c) / XW;
+                    q = a0 + 4 * c - r * XW;
+                }
+                const float* rx = x + (static_cast<int64_t>(b + r) * H + h) * L;
                 float4 v;
                 if (vec_ok && q >= 0 && q + 3 < L) {
                     v = ld_nc_v4(rx + q);
@@ -112,8 +131,15 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
             __syncthreads();
 #pragma unroll 2
             for (int s = 0; s < Geo::SPT; ++s) {
-                const int tl = (s * Geo::NTS + ts) * kTB;
-                if (t0 + tl < L) {
+                int tl = (s * Geo::NTS + ts) * kTB;
+                bool live = t0 + tl < L;
+                int xsh = 0;
+                if (MR) {
+                    const int r = tl / Lp;
+                    live = r < nr && tl - r * Lp < L;
+                    xsh = r * (XW - Lp);
+                }
+                if (live) {
                     float gv[kTB];
 #pragma unroll
                     for (int c = 0; c < kTB / 4; ++c) {
@@ -127,7 +153,7 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
 #pragma unroll
                     for (int c = 0; c < Geo::NVX; ++c) {
                         const float4 q = *reinterpret_cast<const float4*>(
-                            xs + pad_idx(tl + jg * kJR + 4 * c));
+                            xs + pad_idx(tl + xsh + jg * kJR + 4 * c));
                         xv[4 * c + 0] = q.x;
                         xv[4 * c + 1] = q.y;
                         xv[4 * c + 2] = q.z;
@@ -406,11 +432,19 @@ ks_status launch_hier_s(int s, const float* gy, const float* x, float* part, int
                         int64_t H, int64_t L, int64_t K, const HierPlan& pl, cudaStream_t st) {
     const unsigned blocks = static_cast<unsigned>(int64_t(pl.g) * H * pl.njt);
     const int p = static_cast<int>(K / 2);
+    // rows of at most 512: items of several whole rows (-35..-69% at L = 250 / 500;
+    // at L = 1000 two rows per item measured 4% slower, gpurun_out/ab_head_generic)
+    const bool mr = L <= 512;
 #define KS_HIER_CASE(SV)                                                                  \
     case SV:                                                                              \
-        launch_kernel(dw_hier_stage1<NJ, SV, FUSED>, blocks, kDwThreads, 0, st,                      \
-            gy, x, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L),   \
-            static_cast<int>(K), p, pl.g, pl.njt);                                        \
+        if (mr)                                                                           \
+            launch_kernel(dw_hier_stage1<NJ, SV, FUSED, true>, blocks, kDwThreads, 0, st,  \
+                gy, x, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L), \
+                static_cast<int>(K), p, pl.g, pl.njt);                                    \
+        else                                                                              \
+            launch_kernel(dw_hier_stage1<NJ, SV, FUSED, false>, blocks, kDwThreads, 0, st, \
+                gy, x, part, static_cast<int>(B), static_cast<int>(H), static_cast<int>(L), \
+                static_cast<int>(K), p, pl.g, pl.njt);                                    \
         break;
     switch (s) {
         KS_HIER_CASE(0)
