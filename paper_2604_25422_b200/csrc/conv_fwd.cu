@@ -235,7 +235,7 @@ ks_status conv_stencil_f32(const float* in, const float* k, float* out, int64_t 
         const ks_status s = stencil_rows_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
         if (handled) return s;
     }
-    if (!tma_disabled() && K <= 16 && L >= 256) {  // short kernels: register windows, 256-bit stores
+    if (!tma_disabled() && K <= 32 && L >= 256) {  // short kernels: register windows, 256-bit stores
         bool handled = false;
         const ks_status s = stencil_ldg_f32(in, k, out, B, H, L, K, off, reverse, mode, st, &handled);
         if (handled) return s;

@@ -41,7 +41,9 @@ __device__ __forceinline__ void st_v8(float* p, const float (&d)[8]) {
 // V8: L % 8 == 0 and a 32-byte aligned output -- one 256-bit store per
 // thread; otherwise (L % 8 == 4) two 128-bit stores, the second dropped for
 // the last half-block of a row.
-template <int KT, bool FUSED, bool REV, bool V8>
+// MRW: rows shorter than 1024, several whole rows per CTA (a template switch:
+// the runtime branch cost the single-row Separate kernel 8% at K = 7).
+template <int KT, bool FUSED, bool REV, bool V8, bool MRW>
 __global__ void __launch_bounds__(256)
 stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* __restrict__ out, int tpr, int H,
             int L, int rows, int rpc, int tprow) {
@@ -53,7 +55,7 @@ stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* 
     // Rows shorter than 1024 (rpc > 1): a CTA takes rpc whole rows, tprow =
     // ceil(L / 8) threads each, instead of leaving most of its threads idle.
     int row, t;
-    if (rpc > 1) {
+    if constexpr (MRW) {
         const int r = static_cast<int>(threadIdx.x) / tprow;
         row = static_cast<int>(blockIdx.x) * rpc + r;
         t = 8 * (static_cast<int>(threadIdx.x) - r * tprow);
@@ -64,10 +66,11 @@ stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* 
     }
     if (t >= L) return;
     const int h = row % H;
-    float w[16];
+    constexpr int KPS = KT <= 16 ? 16 : 32;  // prepared taps per channel
+    float w[KPS];
 #pragma unroll
     for (int c = 0; c < (KT + 3) / 4; ++c) {
-        const float4 q = __ldg(kp + h * 4 + c);
+        const float4 q = __ldg(kp + h * (KPS / 4) + c);
         w[4 * c + 0] = q.x;
         w[4 * c + 1] = q.y;
         w[4 * c + 2] = q.z;
@@ -111,13 +114,16 @@ ks_status launch_k(bool fused, const float* in, const float4* kp, float* out, in
     const unsigned grid = static_cast<unsigned>(rpc > 1 ? (rows + rpc - 1) / rpc : rows * tpr);
     const int h = static_cast<int>(H), l = static_cast<int>(L), nr = static_cast<int>(rows);
     const bool v8 = L % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
-    if (v8) {
-        if (fused) launch_kernel(stencil_ldg<KT, true, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
-        else launch_kernel(stencil_ldg<KT, false, REV, true>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
+#define KS_LDG_LAUNCH(F, V, M) \
+    launch_kernel(stencil_ldg<KT, F, REV, V, M>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow)
+    if (rpc > 1) {
+        if (v8) { if (fused) KS_LDG_LAUNCH(true, true, true); else KS_LDG_LAUNCH(false, true, true); }
+        else { if (fused) KS_LDG_LAUNCH(true, false, true); else KS_LDG_LAUNCH(false, false, true); }
     } else {
-        if (fused) launch_kernel(stencil_ldg<KT, true, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
-        else launch_kernel(stencil_ldg<KT, false, REV, false>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow);
+        if (v8) { if (fused) KS_LDG_LAUNCH(true, true, false); else KS_LDG_LAUNCH(false, true, false); }
+        else { if (fused) KS_LDG_LAUNCH(true, false, false); else KS_LDG_LAUNCH(false, false, false); }
     }
+#undef KS_LDG_LAUNCH
     return check_launch();
 }
 
@@ -129,7 +135,10 @@ ks_status launch_any(int64_t K, bool fused, const float* in, const float4* kp, f
     case KV: return launch_k<KV, REV>(fused, in, kp, out, rows, H, L, st);
         KS_LDG_CASE(1) KS_LDG_CASE(2) KS_LDG_CASE(3) KS_LDG_CASE(4) KS_LDG_CASE(5) KS_LDG_CASE(6)
         KS_LDG_CASE(7) KS_LDG_CASE(8) KS_LDG_CASE(9) KS_LDG_CASE(10) KS_LDG_CASE(11) KS_LDG_CASE(12)
-        KS_LDG_CASE(13) KS_LDG_CASE(14) KS_LDG_CASE(15) KS_LDG_CASE(16)
+        KS_LDG_CASE(13) KS_LDG_CASE(14) KS_LDG_CASE(15) KS_LDG_CASE(16) KS_LDG_CASE(17) KS_LDG_CASE(18)
+        KS_LDG_CASE(19) KS_LDG_CASE(20) KS_LDG_CASE(21) KS_LDG_CASE(22) KS_LDG_CASE(23) KS_LDG_CASE(24)
+        KS_LDG_CASE(25) KS_LDG_CASE(26) KS_LDG_CASE(27) KS_LDG_CASE(28) KS_LDG_CASE(29) KS_LDG_CASE(30)
+        KS_LDG_CASE(31) KS_LDG_CASE(32)
 #undef KS_LDG_CASE
         default: return KS_ERR_CUDA;
     }
@@ -162,18 +171,23 @@ ks_status stencil_ldg_f32(const float* in, const float* k, float* out, int64_t B
     // K = 16 Separate or L = 256 slower)
     const bool fused_mode = mode == KS_MULADD_FUSED;
     // rows the TMA views cannot take (L % 32 != 0) have no better kernel up to K = 16
-    const int64_t kmax = knob >= 2 || L % 32 != 0 ? 16 : L >= 2048 ? 10 : (fused_mode && L >= 1024) ? 16 : 12;
+    // rows shorter than 1024 (whole rows per CTA): K <= 32 in both modes
+    // (gpurun_out/s25: L = 256 / 512, K = 14..32, -30..-50% against the TMA
+    // kernels; from L = 1024 on, K = 24 / 32 lose by 0-15%)
+    const int64_t kmax = knob >= 2 ? 32 : L < 1024 ? 32 : L % 32 != 0 ? 16 : L >= 2048 ? 10
+                                                     : fused_mode ? 16 : 12;
     if (K > kmax) return KS_OK;
-    if (K < 1 || K > 16 || L % 4 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
+    if (K < 1 || K > 32 || L % 4 != 0 || L >= (int64_t(1) << 30) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;
     if ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (reinterpret_cast<uintptr_t>(out) & 15) != 0) return KS_OK;
     const int64_t rows = B * H;
     if (rows * ((L + 2047) / 2048) >= (int64_t(1) << 31)) return KS_OK;
     float* kp = nullptr;
-    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * 16, st));
+    const int64_t kps = K <= 16 ? 16 : 32;  // the kernel's KPS
+    ks_status rc = cuda_status(scratch_alloc(reinterpret_cast<void**>(&kp), sizeof(float) * H * kps, st));
     if (rc != KS_OK) return rc;
     *handled = true;
-    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * 16 + 255) / 256, 4096)), 256, 0, st, k, kp, H, K, 16,
+    launch_kernel(prep_taps, static_cast<unsigned>(std::min<int64_t>((H * kps + 255) / 256, 4096)), 256, 0, st, k, kp, H, K, kps,
                                                                                                    reverse, 0);
     rc = check_launch();
     if (rc == KS_OK) {

@@ -73,7 +73,8 @@ def logical_traffic(path: str, B: int, H: int, L: int, K: int) -> int:
 def _stencil_tier(L: int, K: int, B: int = 1):
     if L < 1024 and L % 4 == 0 and L + K - 1 <= 252:
         return "stencil_rows", 16, None
-    if L % 4 == 0 and L >= 256 and (K <= 10 or (L < 2048 and K <= 12) or (L % 32 != 0 and K <= 16)):
+    if L % 4 == 0 and L >= 256 and (K <= 10 or (L < 2048 and K <= 12) or (L % 32 != 0 and K <= 16)
+                                     or (L < 1024 and K <= 32)):
         # Separate mode's rule (stencil_ldg_f32)
         return "stencil_ldg", 8, 256  # stencil_ldg.cu: CTA = (row, 2048-output tile), register windows
     if L % 32 != 0 or K > 8192:

@@ -390,7 +390,7 @@ def test_bwd_short_equals_generic_kernels(K):
         assert same(dx_s, host(ks.backward_input(gy, k, m))), m
 
 
-@pytest.mark.parametrize("K", list(range(1, 17)))
+@pytest.mark.parametrize("K", list(range(1, 17)) + [20, 24, 31, 32])
 def test_stencil_short_equals_generic_and_oracle(K, oracle):
     """The three short-kernel forward / dX implementations -- register windows
     with 256-bit stores (stencil_ldg, the default for K <= 10, forced for every
@@ -421,7 +421,8 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
                                    (8, 4, 992, 1000), (6, 5, 64, 500), (40, 6, 256, 7), (20, 4, 512, 12),
                                    (12, 3, 1024, 16), (9, 2, 1984, 13), (30, 3, 256, 16), (7, 5, 500, 7),
                                    (5, 3, 1000, 12), (3, 7, 4092, 5), (4, 3, 2052, 9), (5, 3, 1000, 16),
-                                   (7, 5, 500, 14), (33, 3, 260, 5)])
+                                   (7, 5, 500, 14), (33, 3, 260, 5), (16, 5, 512, 20), (12, 4, 256, 27),
+                                   (9, 3, 992, 31), (11, 2, 500, 32)])
 def test_mid_length_rows_register_tiles(oracle, shape):
     """Rows shorter than 2048 that the whole-row kernels (stencil_rows) do
     not take: stencil_tma's R = 4 tiles sized to the row (32..256 threads),

@@ -5,6 +5,8 @@ O=gpurun_out/ev; mkdir -p $O
 T="timeout 900"
 $T python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 python tools/dump_plans.py $O/plans.json > $O/plans.log 2>&1
+# the suite below checks the library against the plans it just dumped (collect_evidence.sh commits them)
+[ -s $O/plans.json ] && cp $O/plans.json profiles/r02_plans.json
 python tools/b200_device_spec.py $O/b200_device_spec.json > $O/spec.log 2>&1
 # HBM streaming rate per read:write mix (the roof each HBM-bound path is judged against)
 [ -x tools/probes/hbm_mix_probe ] && timeout 120 tools/probes/hbm_mix_probe > $O/hbm_mix.log 2>&1
