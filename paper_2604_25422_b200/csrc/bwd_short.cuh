@@ -94,7 +94,8 @@ struct Geo {
     static constexpr int NV2 = (S2 + 8 + KT - 1 + 3) / 4; // stencil window quads per block
     static constexpr int GYP = BASE == kDW ? 64 : 66;     // stencil input: one halo piece each side
     static constexpr int GYRegion = (GYP * kPitch + 127) / 128 * 128;
-    static constexpr int TapBytes = BASE >= kFWD ? 128 : 0;  // stencils: the row's 16 taps ride in the stage
+    static constexpr int NW = KT <= 16 ? 16 : 32;             // stencil taps per prepared row (kp stride)
+    static constexpr int TapBytes = BASE >= kFWD ? 4 * 32 : 0;  // stencils: the row's NW taps ride in the stage
     // multi-row items: each row's x window carries its own two halo pieces
     static constexpr int XRegion = MR ? ((64 + 2 * kMaxRPI) * kPitch + 127) / 128 * 128 : kXRegion;
     static constexpr int Stage = GYRegion + (HAS_DW ? XRegion : 0) + TapBytes;
@@ -104,7 +105,7 @@ struct Geo {
                                         : KS_DW_NS_LONG;  // dW as dw_tma: 4 stages when FMAs are light
     static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : 3;
     static constexpr uint32_t TX =
-        static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 64 : 0));
+        static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 4 * NW : 0));
     static constexpr bool HAS_OBUF = HAS_ST && !DST;  // output tiles leave by TMA store from shared memory
     static constexpr int Smem = (HAS_OBUF ? 2 * kOutBytes : 0) + NS * Stage + 64 + 1024;
     static_assert(QS % 4 == 0 && QS + 8 <= 4 * NV2, "gy block inside the dX window");
@@ -139,7 +140,7 @@ struct Args {
 template <int KT, bool FUSED, int MODE, int C0>
 __device__ __forceinline__ void item(const unsigned char* gys, int xshift, unsigned char* ob, uint32_t o0, uint32_t o1,
                                      float* gout,
-                                     const float (&w)[Geo<KT, MODE>::HAS_ST ? 16 : 1],
+                                     const float (&w)[Geo<KT, MODE>::HAS_ST ? Geo<KT, MODE>::NW : 1],
                                      float (&acc)[Geo<KT, MODE>::HAS_DW ? KT : 1]) {
     using Gm = Geo<KT, MODE>;
     float gv[8];
@@ -238,7 +239,8 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
         tma_load_3d(sb, in_map, 0, it0 / 32 - (Gm::BASE == kDW ? 0 : 1), irow, bar);
         if constexpr (Gm::HAS_DW) tma_load_3d(sb + Gm::GYRegion, x_map, 0, it0 / 32 - Gm::XR0, irow, bar);
 #endif
-        if constexpr (Gm::BASE >= kFWD) bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * 16, 64, bar);
+        if constexpr (Gm::BASE >= kFWD)
+            bulk_load(sb + Gm::GYRegion, k + static_cast<int64_t>(irow % a.H) * Gm::NW, 4 * Gm::NW, bar);
         it0 += kTT;
         if (it0 >= a.L) {
             it0 = 0;
@@ -251,7 +253,7 @@ __device__ __forceinline__ void run(const CUtensorMap* in_map, const CUtensorMap
     // stencil taps: the fused backward holds the CTA's reversed row in
     // registers; the stencils read the row's prepared taps (prep_taps:
     // reversed for dX, zero past K) from each stage
-    float w[Gm::HAS_ST ? 16 : 1];
+    float w[Gm::HAS_ST ? Gm::NW : 1];
     if constexpr (Gm::BASE == kFUSED) {
 #pragma unroll
         for (int jj = 0; jj < KT; ++jj) w[jj] = k[static_cast<int64_t>(a.h) * KT + KT - 1 - jj];

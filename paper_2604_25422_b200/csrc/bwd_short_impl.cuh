@@ -25,8 +25,10 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
     // short and the hardware scheduler's rebalancing of many CTAs pays
     // (round-2 ABAB, gpurun_out/s8: (64,1024,16384,16) fwd 1.50 -> 1.27 ms,
     // config 5a fwd 11.8 -> 10.9 ms; Separate 1-9% slower with it)
+    // (rows of at least two items: with one 2048-wide item per row a per-row
+    // CTA has nothing to prefetch -- (1024,64,2048,K) lost 38-55%, s28)
     const int64_t rows_opt = opt(kOptStsRows);
-    const bool per_row = rows_opt == 1 || (rows_opt < 0 && FUSED);
+    const bool per_row = rows_opt == 1 || (rows_opt < 0 && FUSED && L >= 2 * kTT);
     const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H
                            : per_row ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
     launch_kernel(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
@@ -54,6 +56,23 @@ ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorM
         KS_BWDS_CASE(1) KS_BWDS_CASE(2) KS_BWDS_CASE(3) KS_BWDS_CASE(4) KS_BWDS_CASE(5) KS_BWDS_CASE(6)
         KS_BWDS_CASE(7) KS_BWDS_CASE(8) KS_BWDS_CASE(9) KS_BWDS_CASE(10) KS_BWDS_CASE(11) KS_BWDS_CASE(12)
         KS_BWDS_CASE(13) KS_BWDS_CASE(14) KS_BWDS_CASE(15) KS_BWDS_CASE(16)
+#undef KS_BWDS_CASE
+        default: return KS_ERR_CUDA;
+    }
+}
+
+// The stencils (MODE kFWD / kDXS) also take 16 < K <= 32 (dW and the fused
+// backward stay at K <= 16).
+template <int MODE>
+ks_status launch_any_k_st(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& om, const float* kp,
+                          int64_t B, int64_t H, int64_t L, float* out, cudaStream_t st) {
+    if (K <= 16) return launch_any_k<MODE>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
+    switch (K) {
+#define KS_BWDS_CASE(KV) \
+    case KV: return launch_m<KV, MODE>(f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
+        KS_BWDS_CASE(17) KS_BWDS_CASE(18) KS_BWDS_CASE(19) KS_BWDS_CASE(20) KS_BWDS_CASE(21) KS_BWDS_CASE(22)
+        KS_BWDS_CASE(23) KS_BWDS_CASE(24) KS_BWDS_CASE(25) KS_BWDS_CASE(26) KS_BWDS_CASE(27) KS_BWDS_CASE(28)
+        KS_BWDS_CASE(29) KS_BWDS_CASE(30) KS_BWDS_CASE(31) KS_BWDS_CASE(32)
 #undef KS_BWDS_CASE
         default: return KS_ERR_CUDA;
     }

@@ -648,7 +648,12 @@ ks_status stencil_pad_f32(const float* in, const float* k, float* out, int64_t B
     // gpurun_out/s10: config 4 fwd 9.50 -> 8.95 ms, dX 9.13 -> 8.93, 5b shard
     // fwd 10.01 -> 9.57), Fused mode and K >= 1024 keep this kernel (Fused
     // config 4 fwd 4.35 vs 5.80 ms).  Option stencil_pad = 2 forces it.
-    if (mode != KS_MULADD_FUSED && K < 1024 && opt(kOptStencilPad) < 2) return KS_OK;
+    if ((mode != KS_MULADD_FUSED && K < 1024) || K < 48) {
+        // (and in Fused mode below K = 48, where a padded tile's 64 computed
+        // taps outweigh the register tiles: K = 40 fwd 0.346 -> 0.318 ms,
+        // gpurun_out/s27; from K = 48 on this kernel is ahead)
+        if (opt(kOptStencilPad) < 2) return KS_OK;
+    }
     g.mirror = 0;  // set below, once the tile width is known
     g.RPT = 1;
     while (g.RPT < 4 && static_cast<int64_t>(NT * kR / (2 * g.RPT)) >= L && H % (2 * g.RPT) == 0) g.RPT *= 2;

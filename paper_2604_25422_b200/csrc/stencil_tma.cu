@@ -256,7 +256,13 @@ ks_status stencil_tma_f32(const float* in, const float* k, float* out, int64_t B
         const ks_status s = stencil_pad_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }
-    if (K <= 16 && L >= 1024 && opt(kOptSts)) {  // K-specialised short-kernel stencil (bwd_short.cuh)
+    // K-specialised stencil (bwd_short.cuh): K <= 16, and 16 < K <= 28 in
+    // Separate mode / K <= 32 in Fused mode on rows of 4096 or more (round-2
+    // ABAB against these register tiles, gpurun_out/s28: Separate K = 17..28
+    // -8..-14%, K = 32 +10%; Fused L >= 8192 K = 20..32 -8..-15%)
+    const int64_t sts = opt(kOptSts);
+    const int64_t kmax_sts = sts >= 2 ? 32 : sts == 0 ? 0 : mode == KS_MULADD_FUSED ? (L >= 4096 ? 32 : 16) : 28;
+    if (K <= kmax_sts && L >= 1024) {
         const ks_status s = stencil_short_f32(in, k, out, B, H, L, K, off, reverse, mode, st, handled);
         if (*handled) return s;
     }

@@ -86,7 +86,7 @@ def _stencil_tier(L: int, K: int, B: int = 1):
     # Separate mode (the reference's default, which this model and the committed
     # plans follow) below K = 1024: stencil_tma's register tiles (Fused mode
     # takes stencil_pad here too)
-    if K <= 16 and L >= 1024:
+    if K <= 28 and L >= 1024:  # Separate mode's rule (stencil_tma_f32)
         return "stencil_short", 8, 256  # bwd_short.cuh MODE fwd/dX: 2048-output tiles, persistent
     if K > 32 and L >= 2048:  # stencil_tma.cu pick_tile
         return "stencil_tma", 32, 256 if L >= 8192 else 128 if L >= 4096 else 64

@@ -404,7 +404,7 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
     kh = k.cpu().numpy()
     for m in (SEPARATE, FUSED):
         res = []
-        for opts in ({"ldg": 2}, {"ldg": 0}, {"ldg": 0, "sts": 0}):
+        for opts in ({"ldg": 2}, {"ldg": 0}, {"ldg": 0, "sts": 0}, {"ldg": 0, "sts": 2}):
             with ks.options(**opts):
                 res.append((host(ks.forward(x, k, m)), host(ks.backward_input(gy, k, m))))
         for y_o, dx_o in res[1:]:
