@@ -103,7 +103,7 @@ struct Geo {
                               : MR ? 3
                               : KT <= 8 ? (BASE == kFUSED ? KS_FUSED_NS_SHORT : KS_DW_NS_SHORT)
                                         : KS_DW_NS_LONG;  // dW as dw_tma: 4 stages when FMAs are light
-    static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : 3;
+    static constexpr int MinBlocks = BASE >= kFWD ? KS_ST_MINB : KT > 16 ? 2 : 3;  // dW with 32 accumulators: 2
     static constexpr uint32_t TX =
         static_cast<uint32_t>(GYP * kPitch + (HAS_DW ? kXP * kPitch : 0) + (BASE >= kFWD ? 4 * NW : 0));
     static constexpr bool HAS_OBUF = HAS_ST && !DST;  // output tiles leave by TMA store from shared memory

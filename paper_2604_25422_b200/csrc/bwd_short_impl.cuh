@@ -61,15 +61,16 @@ ks_status launch_any_k(int64_t K, bool f, const CUtensorMap& im, const CUtensorM
     }
 }
 
-// The stencils (MODE kFWD / kDXS) also take 16 < K <= 32 (dW and the fused
-// backward stay at K <= 16).
+// The stencils (MODE kFWD / kDXS) and dW (kDW) also take 16 < K <= 32 (the
+// fused backward stays at K <= 16).
 template <int MODE>
-ks_status launch_any_k_st(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& om, const float* kp,
-                          int64_t B, int64_t H, int64_t L, float* out, cudaStream_t st) {
-    if (K <= 16) return launch_any_k<MODE>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
+ks_status launch_any_k32(int64_t K, bool f, const CUtensorMap& im, const CUtensorMap& xm, const CUtensorMap& om,
+                         const float* k, float* part, int64_t B, int64_t H, int64_t L, int G, float* out,
+                         cudaStream_t st, int rpi = 0) {
+    if (K <= 16) return launch_any_k<MODE>(K, f, im, xm, om, k, part, B, H, L, G, out, st, rpi);
     switch (K) {
 #define KS_BWDS_CASE(KV) \
-    case KV: return launch_m<KV, MODE>(f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
+    case KV: return launch_m<KV, MODE>(f, im, xm, om, k, part, B, H, L, G, out, st, rpi);
         KS_BWDS_CASE(17) KS_BWDS_CASE(18) KS_BWDS_CASE(19) KS_BWDS_CASE(20) KS_BWDS_CASE(21) KS_BWDS_CASE(22)
         KS_BWDS_CASE(23) KS_BWDS_CASE(24) KS_BWDS_CASE(25) KS_BWDS_CASE(26) KS_BWDS_CASE(27) KS_BWDS_CASE(28)
         KS_BWDS_CASE(29) KS_BWDS_CASE(30) KS_BWDS_CASE(31) KS_BWDS_CASE(32)
@@ -90,7 +91,7 @@ inline bool direct_store(const float* out) {
 }
 
 inline bool shape_ok(int64_t B, int64_t H, int64_t L, int64_t K) {
-    return K >= 1 && K <= 16 && L % 32 == 0 && B * H < (int64_t(1) << 31) && L < (int64_t(1) << 30);
+    return K >= 1 && K <= 32 && L % 32 == 0 && B * H < (int64_t(1) << 31) && L < (int64_t(1) << 30);
 }
 
 // dW (DX = false) or the fused backward (DX = true).  *handled = false: shape
@@ -99,7 +100,7 @@ template <bool DX>
 ks_status launch_bwd_short(const float* gy, const float* x, const float* k, float* dx, float* part, int64_t B,
                            int64_t H, int64_t L, int64_t K, int G, int mode, cudaStream_t st, bool* handled) {
     *handled = false;
-    if (!shape_ok(B, H, L, K) || int64_t(G) * H >= (int64_t(1) << 31)) return KS_OK;
+    if (!shape_ok(B, H, L, K) || (DX && K > 16) || int64_t(G) * H >= (int64_t(1) << 31)) return KS_OK;
     CUtensorMap gm, xm, dm;
     if constexpr (!DX) {
         // rows shorter than a 2048-wide item: items of RPI whole rows of the
@@ -110,7 +111,7 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
             if (!encode_padded_view(&gm, gy, B * H, L, H, npr, 1, rpi)) return KS_OK;
             if (!encode_padded_view(&xm, x, B * H, L, H, npr + 2, 1, rpi)) return KS_OK;
             *handled = true;
-            return launch_any_k<kDW | kMRow>(K, true, gm, xm, gm, k, part, B, H, L, G, nullptr, st, rpi);
+            return launch_any_k32<kDW | kMRow>(K, true, gm, xm, gm, k, part, B, H, L, G, nullptr, st, rpi);
         }
     }
     if (!encode_row_view_padded(&gm, gy, B * H, L, DX ? 66 : 64)) return KS_OK;
@@ -122,7 +123,7 @@ ks_status launch_bwd_short(const float* gy, const float* x, const float* k, floa
     }
     *handled = true;
     const bool f = mode == KS_MULADD_FUSED;
-    if constexpr (!DX) return launch_any_k<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, nullptr, st);
+    if constexpr (!DX) return launch_any_k32<kDW>(K, f, gm, xm, dm, k, part, B, H, L, G, nullptr, st);
     else return direct_store(dx) ? launch_any_k<kFUSED | kDirect>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st)
                             : launch_any_k<kFUSED>(K, f, gm, xm, dm, k, part, B, H, L, G, dx, st);
 }

@@ -11,7 +11,7 @@ static ks_status launch_stencil_short(const float* in, const float* k, float* ou
                                       bool* handled) {
     *handled = false;
     // stencils: 1 <= K <= 32 (the shape envelope of dW / the fused backward is K <= 16)
-    if (K < 1 || K > 32 || !shape_ok(B, H, L, std::min<int64_t>(K, 16)) || off != (reverse ? K - 1 - K / 2 : K / 2))
+    if (!shape_ok(B, H, L, K) || off != (reverse ? K - 1 - K / 2 : K / 2))
         return KS_OK;
     CUtensorMap im, om;
     if (!encode_row_view_padded(&im, in, B * H, L, 66)) return KS_OK;
@@ -27,11 +27,11 @@ static ks_status launch_stencil_short(const float* in, const float* k, float* ou
     if (rc == KS_OK) {
         const bool f = mode == KS_MULADD_FUSED;
         if (direct_store(out))
-            rc = reverse ? launch_any_k_st<kDXS | kDirect>(K, f, im, om, kp, B, H, L, out, st)
-                         : launch_any_k_st<kFWD | kDirect>(K, f, im, om, kp, B, H, L, out, st);
+            rc = reverse ? launch_any_k32<kDXS | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st)
+                         : launch_any_k32<kFWD | kDirect>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
         else
-            rc = reverse ? launch_any_k_st<kDXS>(K, f, im, om, kp, B, H, L, out, st)
-                         : launch_any_k_st<kFWD>(K, f, im, om, kp, B, H, L, out, st);
+            rc = reverse ? launch_any_k32<kDXS>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st)
+                         : launch_any_k32<kFWD>(K, f, im, im, om, kp, nullptr, B, H, L, 1, out, st);
     }
     scratch_free(kp, st);
     return rc;

@@ -384,9 +384,11 @@ ks_status bwd_short_fused_stage1(const float*, const float*, const float*, float
 
 // K <= 16: the K-specialised kernels of bwd_short.cuh (same bits, fewer
 // instructions) unless an A/B knob asks for this file's generic kernel.
+// dW up to K = 32 (round 2, gpurun_out/s30: K = 17..32 -11..-40% against this
+// file's kernel, e.g. (256,512,8192,24) 2.21 -> 1.32 ms); the fused backward
+// checks K <= 16 itself.
 static bool use_bwd_short(int64_t K) {
-    if (K > 16) return false;
-    if (opt(kOptBwds) == 0) return false;
+    if (opt(kOptBwds) == 0 || K > 32) return false;
     return opt(kOptDwtmaNs) == 0 && opt(kOptDwtmaJ16) != 0;
 }
 

@@ -29,7 +29,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"disable_tma", 0, 0, 1},    // 1: generic (non-TMA) kernels only
     {"ldg", 1, 0, 2},            // stencil_ldg for fwd/dX (L >= 256): 0 never, 1 auto (K <= 10; L < 2048: K <= 12, Fused K <= 16 from L = 1024; L < 1024: K <= 32), 2 K <= 32
     {"sts", 1, 0, 2},            // fwd/dX through bwd_short: 0 never (stencil_tma), 1 auto (K <= 16; Separate K <= 28, Fused K <= 32 from L = 4096), 2 K <= 32
-    {"bwds", 1, 0, 1},           // K <= 16 dW / fused backward through bwd_short (0: dw_tma)
+    {"bwds", 1, 0, 1},           // dW (K <= 32) / fused backward (K <= 16) through bwd_short (0: dw_tma)
     {"dst", 0, 0, 1},            // bwd_short stencil outputs by 256-bit stores instead of TMA stores
     {"dwtma_j16", 1, 0, 1},      // dw_tma: one 16-tap group for 8 < K <= 16 (0: two 8-tap groups)
     {"dwtma_ns", 0, 0, 6},       // dw_tma stages (0: auto)

@@ -123,7 +123,7 @@ def _dw_groups(B: int, H: int, L: int, K: int) -> tuple[str, int]:
     G = max(1, min(math.ceil(target / (H * njt)), B))
     if L < 2048 and L % 4 == 0 and L + 8 * min(8, groups8) + 16 <= 252:  # dw_rows: a whole row in one TMA box
         return "dw_rows", G
-    if L % 32 == 0 and K <= 16:
+    if L % 32 == 0 and K <= 32:
         return "dw_short", G  # bwd_short.cuh MODE dW: dw_tma's decomposition, K-specialised
     return ("dw_tma" if L % 32 == 0 else "dw_hier_stage1"), G
 

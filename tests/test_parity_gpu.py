@@ -483,6 +483,27 @@ def test_dw_pad_below_128_taps(oracle, shape):
         assert normwise(dk0[h:h + 1], truth) <= HIER_TOL, h
 
 
+@pytest.mark.parametrize("shape", [(20, 8, 4096, 24), (9, 5, 2080, 17), (12, 4, 8192, 32), (30, 3, 512, 20),
+                                   (11, 3, 1024, 31)])
+def test_dw_short_kernel_up_to_32_taps(oracle, shape):
+    """HIERARCHICAL dW through the K-specialised kernel for 16 < K <= 32 (the
+    default; multi-row items on the short rows) and through dw_tma (option
+    bwds = 0): dk within the tolerance of fp64 on every channel, run-to-run
+    bitwise."""
+    B, H, L, K = shape
+    x, k, gy = ks.make_inputs(23, B, H, L, K)
+    dk = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+    assert same(dk, host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, SEPARATE)))
+    with ks.options(bwds=0):
+        dk0 = host(ks.backward_weight(gy, x, K, ks.HIERARCHICAL, 0, FUSED))
+    xh, gh = host(x), host(gy)
+    for h in range(H):
+        xs, gs = np.ascontiguousarray(xh[:, h:h + 1]), np.ascontiguousarray(gh[:, h:h + 1])
+        truth = oracle.backward_weight(gs.astype(np.float64), xs.astype(np.float64), K, SEQUENTIAL)
+        assert normwise(dk[h:h + 1], truth) <= HIER_TOL, h
+        assert normwise(dk0[h:h + 1], truth) <= HIER_TOL, h
+
+
 @pytest.mark.parametrize("K", [1, 4, 7, 10, 13, 16])
 def test_short_kernels_both_output_paths(K):
     """The short-kernel stencils and fused backward write their outputs either

@@ -50,10 +50,13 @@ for (B, H, L, K) in shapes:
 # (40,2,2048,1030), (32,3,1024,700): K comparable to L with >= 32 batch rows ->
 # the batch-lane stencil (piece ring wraps several times, ragged row group, S = 1..3)
 # (37,6,256,7), (13,3,1024,12): K <= 16 dW on rows shorter than an item -> items of
-# whole rows (ragged last item); (24,8,256,32): stencil_tma R = 4 tiles sized to the row
+# whole rows (ragged last item); (24,8,256,32): short rows through stencil_ldg's
+# whole-row CTAs; (20,4,2048,24), (9,3,512,20), (6,4,4096,28): bwd_short dW and
+# stencils for 16 < K <= 32
 for (B, H, L, K) in [(32, 64, 2048, 64), (32, 256, 2048, 128), (4, 8, 4096, 150), (64, 32, 4096, 7), (2400, 16, 48, 48),
                      (40, 16, 2080, 16), (8, 4, 4160, 13), (2, 4, 4096, 4096), (3, 8, 1024, 1024),
-                     (40, 2, 2048, 1030), (32, 3, 1024, 700), (37, 6, 256, 7), (13, 3, 1024, 12), (24, 8, 256, 32)]:
+                     (40, 2, 2048, 1030), (32, 3, 1024, 700), (37, 6, 256, 7), (13, 3, 1024, 12), (24, 8, 256, 32),
+                     (20, 4, 2048, 24), (9, 3, 512, 20), (6, 4, 4096, 28)]:
     x, k, gy = o.fill_inputs(5, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
     y = ks.forward(dx_, dk_, 1)
