@@ -262,6 +262,20 @@ ks_status ks_dwconv1d_dw_allreduce_f32(float* dk, int64_t H, int64_t K, ks_comm*
  * bits for a given world size. */
 ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, int64_t K,
                                            ks_comm* comm, void* stream);
+/* Sharded CHUNKED(chunk) dW, bitwise the single-device
+ * ks_dwconv1d_dw_f32(KS_DW_CHUNKED, chunk) of the whole batch -- the
+ * reference's reduce_chunked (src/conv_core.cpp:122-146) with its chunks
+ * spread over the ranks, so the bits do not depend on the number of GPUs
+ * (SURVEY 8(e)'s G-invariant option).  Rank r holds global rows
+ * [b0, b0 + B_local) of B_total; the ranks' rows must tile [0, B_total) in
+ * rank order with every rank boundary (row * L) a multiple of `chunk`, else
+ * KS_ERR_SHARD.  Each rank computes the partials of its own chunks, they are
+ * all-gathered (rank order = global chunk order) and every rank adds them in
+ * chunk order.  dk[H,K] is written on every rank.  Synchronous on a host
+ * communicator; on an NCCL communicator the gather runs on `stream`. */
+ks_status ks_dwconv1d_dw_chunked_sharded_f32(const float* gy, const float* x, float* dk, int64_t B_local,
+                                             int64_t b0, int64_t B_total, int64_t H, int64_t L, int64_t K,
+                                             int64_t chunk, int mode, ks_comm* comm, void* stream);
 /* out[i] = the midpoint-split pairwise tree over gather[r * n + i], r = 0 ..
  * world-1 (the reference's reduce_pairwise shape, src/conv_core.cpp:113-118,
  * over ranks); 1 <= world <= 64. */

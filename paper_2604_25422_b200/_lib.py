@@ -40,6 +40,7 @@ EXPORTED = [
     "ks_shard_rows", "ks_comm_unique_id", "ks_comm_init", "ks_comm_init_host", "ks_comm_destroy",
     "ks_comm_allgather_host",
     "ks_dwconv1d_dw_allreduce_f32", "ks_dwconv1d_dw_allgather_sum_f32", "ks_rank_tree_sum_f32",
+    "ks_dwconv1d_dw_chunked_sharded_f32",
     "ks_peer_create", "ks_peer_destroy", "ks_dwconv1d_dw_f32_peer", "ks_peer_timed_out",
 ]
 
@@ -82,6 +83,8 @@ _SIGS = {
     "ks_comm_destroy": ([_p], _int),
     "ks_dwconv1d_dw_allreduce_f32": ([_p, _i64, _i64, _p, _p], _int),
     "ks_dwconv1d_dw_allgather_sum_f32": ([_p, _p, _i64, _i64, _p, _p], _int),
+    "ks_dwconv1d_dw_chunked_sharded_f32": ([_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _i64, _i64, _int, _p, _p],
+                                           _int),
     "ks_peer_create": ([_p, _sz, C.POINTER(_p)], _int),
     "ks_peer_destroy": ([_p], _int),
     "ks_dwconv1d_dw_f32_peer": ([_p, _p, _p, _i64, _i64, _i64, _i64, _i64, _int, _p, _p], _int),

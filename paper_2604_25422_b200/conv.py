@@ -375,6 +375,22 @@ class Comm:
                                                               self.handle, _stream(dk)),
                   "dw_allgather_sum")
 
+    def chunked_dw(self, gy, x, K: int, chunk: int, mode: int, b0: int, B_total: int, out=None):
+        """ks_dwconv1d_dw_chunked_sharded_f32: this rank holds global rows
+        [b0, b0 + B_local) of B_total; dk (every rank) is bitwise the
+        single-device CHUNKED(chunk) dW of the whole batch."""
+        B, H, L = (int(v) for v in gy.shape)
+        if tuple(x.shape) != (B, H, L):
+            raise DimensionError(f"chunked_dw: x shape {tuple(x.shape)} != gy shape {(B, H, L)}")
+        if chunk < 1:
+            raise DimensionError(f"chunked_dw: chunk_size must be >= 1, got {chunk}")
+        out = _check_out(out, gy, (H, K), "chunked_dw: out")
+        with _on_device(gy):
+            check(_lib.lib().ks_dwconv1d_dw_chunked_sharded_f32(_ptr(gy), _ptr(x), _ptr(out), B, b0, B_total, H, L,
+                                                                K, chunk, mode, self.handle, _stream(gy)),
+                  "dw_chunked_sharded")
+        return out
+
     def peer(self, B: int, H: int, L: int, K: int, B_total: int = 0) -> "Peer":
         """Peer-memory dW combine for per-rank shape (B,H,L,K); with B_total the
         global plan (bitwise = the 1-GPU result when the shards align)."""

@@ -537,6 +537,53 @@ static ks_status dw_exact(const T* gy, const T* x, T* dk, int64_t B, int64_t H, 
     return check_launch();
 }
 
+// Sharded CHUNKED(c) support (dist.cu): the partials of `nchunks` chunks of
+// this rank's rows (flat index from the rank's first row), and the total over
+// the gathered partials of every rank in rank order = global chunk order.
+ks_status dw_chunk_partials_f32(const float* gy, const float* x, float* part, int64_t B, int64_t H, int64_t L,
+                                int64_t K, int64_t chunk, int64_t nchunks, int mode, cudaStream_t st) {
+    const int64_t total = nchunks * H * K;
+    if (total == 0) return KS_OK;
+    const unsigned blocks = static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, int64_t(num_sms()) * 64));
+    if (mode == KS_MULADD_FUSED)
+        launch_kernel(dw_chunk_partials<float, true>, blocks, 256, 0, st, gy, x, part, B, H, L, K, chunk, nchunks);
+    else
+        launch_kernel(dw_chunk_partials<float, false>, blocks, 256, 0, st, gy, x, part, B, H, L, K, chunk, nchunks);
+    return check_launch();
+}
+
+struct RankChunks {
+    int n[64];  // chunks held by each rank
+};
+
+// dk[i] = ((0 + p[0]) + p[1]) + ... over every rank's chunks in rank order --
+// dw_chunk_total's order on the global chunk list (one chunk in all: copied).
+__global__ void dw_chunk_total_ranks(const float* __restrict__ gather, float* __restrict__ dk, int64_t HK,
+                                     int world, int ncmax, RankChunks rc) {
+    const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+    if (i >= HK) return;
+    int ntot = 0;
+    for (int r = 0; r < world; ++r) ntot += rc.n[r];
+    float total = 0.f;
+    bool first = true;
+    for (int r = 0; r < world; ++r)
+        for (int c = 0; c < rc.n[r]; ++c) {
+            const float v = gather[(static_cast<int64_t>(r) * ncmax + c) * HK + i];
+            total = (ntot == 1 && first) ? v : total + v;
+            first = false;
+        }
+    dk[i] = total;
+}
+
+ks_status dw_chunk_total_ranks_f32(const float* gather, float* dk, int64_t HK, int world, int ncmax,
+                                   const int* counts, cudaStream_t st) {
+    RankChunks rc{};
+    for (int r = 0; r < world && r < 64; ++r) rc.n[r] = counts[r];
+    launch_kernel(dw_chunk_total_ranks, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, gather, dk, HK, world,
+                  ncmax, rc);
+    return check_launch();
+}
+
 ks_status dw_tma_stage1(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int, int,
                         cudaStream_t, bool*);
 

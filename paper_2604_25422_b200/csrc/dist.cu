@@ -15,6 +15,7 @@
 //    so this is also how the multi-rank paths are exercised on one B200.
 #include <nccl.h>
 
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -107,11 +108,81 @@ static ks_status host_gather_device(ks_comm* c, const float* dk, float* gather, 
     return s;
 }
 
+ks_status dw_chunk_partials_f32(const float*, const float*, float*, int64_t, int64_t, int64_t, int64_t, int64_t,
+                                int64_t, int, cudaStream_t);
+ks_status dw_chunk_total_ranks_f32(const float*, float*, int64_t, int, int, const int*, cudaStream_t);
+
 }  // namespace ks
 
 using namespace ks;
 
 extern "C" {
+
+ks_status ks_dwconv1d_dw_chunked_sharded_f32(const float* gy, const float* x, float* dk, int64_t B_local,
+                                             int64_t b0, int64_t B_total, int64_t H, int64_t L, int64_t K,
+                                             int64_t chunk, int mode, ks_comm* comm, void* stream) {
+    if (!dk || !comm || (B_local > 0 && (!gy || !x))) return KS_ERR_NULL;
+    if (B_total < 1 || B_local < 0 || b0 < 0 || b0 + B_local > B_total) return KS_ERR_DIM_B;
+    if (H < 1) return KS_ERR_DIM_H;
+    if (L < 1) return KS_ERR_DIM_L;
+    if (K < 1) return KS_ERR_DIM_K;
+    if (chunk < 1) return KS_ERR_BAD_CHUNK;
+    if (mode != KS_MULADD_SEPARATE && mode != KS_MULADD_FUSED) return KS_ERR_BAD_MODE;
+    if (comm->world > 64) return KS_ERR_SHARD;
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int world = comm->world;
+    // every rank's rows: they must tile [0, B_total) in rank order, and no
+    // chunk may straddle two ranks (each chunk's chain is computed whole)
+    int64_t mine[2] = {b0, B_local};
+    std::vector<int64_t> all(2 * static_cast<size_t>(world));
+    ks_status s = comm_allgather_host(comm, mine, all.data(), sizeof(mine));
+    if (s != KS_OK) return s;
+    const int64_t n_flat = B_total * L;
+    const int64_t c_eff = std::min(chunk, n_flat);  // chunk >= B*L: one chunk (SEQUENTIAL)
+    std::vector<int> counts(world);
+    int64_t next = 0, ncmax = 0;
+    for (int r = 0; r < world; ++r) {
+        const int64_t rb0 = all[2 * r], rnb = all[2 * r + 1];
+        if (rb0 != next) {
+            set_last_error("sharded CHUNKED dW: ranks' rows must tile [0, B) in rank order");
+            return KS_ERR_SHARD;
+        }
+        const int64_t f0 = rb0 * L, f1 = (rb0 + rnb) * L;
+        if (rnb > 0 && (f0 % c_eff != 0 || (f1 % c_eff != 0 && f1 != n_flat))) {
+            set_last_error("sharded CHUNKED dW: a chunk straddles two ranks (shard rows * L must be multiples of chunk)");
+            return KS_ERR_SHARD;
+        }
+        const int64_t nc = rnb > 0 ? (f1 - f0 + c_eff - 1) / c_eff : 0;
+        if (nc >= (int64_t(1) << 30)) return KS_ERR_SHARD;
+        counts[r] = static_cast<int>(nc);
+        ncmax = std::max(ncmax, nc);
+        next = rb0 + rnb;
+    }
+    if (next != B_total) {
+        set_last_error("sharded CHUNKED dW: ranks' rows must cover [0, B)");
+        return KS_ERR_SHARD;
+    }
+    const int64_t HK = H * K;
+    const size_t n = static_cast<size_t>(std::max<int64_t>(1, ncmax) * HK);
+    float *part = nullptr, *gather = nullptr;
+    s = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&part), n * sizeof(float), st));
+    if (s == KS_OK) s = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&gather), n * world * sizeof(float), st));
+    if (s == KS_OK) s = cuda_status(cudaMemsetAsync(part, 0, n * sizeof(float), st));
+    if (s == KS_OK)
+        s = dw_chunk_partials_f32(gy, x, part, B_local, H, L, K, c_eff, counts[comm->rank], mode, st);
+    if (s == KS_OK)
+        s = comm->host_allgather || world == 1
+                ? (world == 1 ? cuda_status(cudaMemcpyAsync(gather, part, n * sizeof(float), cudaMemcpyDeviceToDevice, st))
+                              : host_gather_device(comm, part, gather, n, st))
+                : nccl_status(ncclAllGather(part, gather, n, ncclFloat, comm->nccl, st));
+    if (s == KS_OK)
+        s = dw_chunk_total_ranks_f32(gather, dk, HK, world, static_cast<int>(std::max<int64_t>(1, ncmax)),
+                                     counts.data(), st);
+    if (gather) cudaFreeAsync(gather, st);
+    if (part) cudaFreeAsync(part, st);
+    return s;
+}
+
 
 ks_status ks_shard_rows(int64_t B, int world, int rank, int64_t* b0, int64_t* nb) {
     if (!b0 || !nb) return KS_ERR_NULL;

@@ -199,3 +199,57 @@ def test_step_host_per_shard_world2(oracle):
     assert same(res[0][2], res[1][2])
     truth = oracle.backward_weight(gy.astype(np.float64), x.astype(np.float64), K, SEQUENTIAL)
     assert normwise(res[0][2], truth) <= HIER_TOL
+
+
+def _chunked_worker(rank, world, results, B, H, L, K, chunk, mode, bounds):
+    import paper_2604_25422_b200 as ks
+    torch.cuda.set_device(0)
+    b0, b1 = bounds[rank], bounds[rank + 1]
+    comm = ks.Comm.host(world, rank, gloo_allgather)
+    try:
+        if b1 > b0:
+            x, k, gy = ks.make_inputs(7, b1 - b0, H, L, K, device="cuda", b0=b0, B_total=B)
+        else:  # a rank without rows still takes part in the exchange
+            x = gy = torch.empty((0, H, L), dtype=torch.float32, device="cuda")
+        try:
+            dk = comm.chunked_dw(gy, x, K, chunk, mode, b0, B)
+            torch.cuda.synchronize()
+            results[rank] = dk.cpu().numpy()
+        except ks.KsError as e:
+            results[rank] = f"error: {e}"
+    finally:
+        comm.close()
+
+
+@pytest.mark.parametrize("case", [
+    # (B, H, L, K, chunk, mode, rank row bounds)
+    (12, 4, 2048, 7, 2048, 1, [0, 4, 8, 12]),        # one row per chunk, 3 ranks
+    (12, 3, 2048, 9, 4096, 0, [0, 6, 12]),           # two rows per chunk
+    (10, 2, 1000, 33, 2000, 1, [0, 4, 10]),          # uneven shards, ragged L
+    (9, 2, 512, 5, 1536, 0, [0, 3, 6, 9]),           # three rows per chunk
+    (8, 2, 300, 7, 100, 1, [0, 0, 8]),               # an empty rank, chunks inside rows
+    (6, 3, 256, 3, 1 << 20, 0, [0, 6, 6]),           # chunk >= B*L: SEQUENTIAL, all rows on rank 0
+])
+def test_chunked_dw_sharded_equals_one_gpu(case):
+    """ks_dwconv1d_dw_chunked_sharded_f32 on 2-3 processes sharing the GPU:
+    every rank's dk is bitwise the single-device CHUNKED(chunk) dW of the whole
+    batch (and so independent of the rank count), uneven and empty shards
+    included."""
+    import paper_2604_25422_b200 as ks
+    B, H, L, K, chunk, mode, bounds = case
+    world = len(bounds) - 1
+    res = run_world(world, _chunked_worker, B, H, L, K, chunk, mode, bounds)
+    x, k, gy = ks.make_inputs(7, B, H, L, K, device="cuda")
+    ref = ks.backward_weight(gy, x, K, ks.CHUNKED, chunk, mode).cpu().numpy()
+    for r in range(world):
+        assert not isinstance(res[r], str), res[r]
+        assert same(res[r], ref), r
+
+
+def test_chunked_dw_sharded_rejects_straddling_chunks():
+    """A chunk that would straddle two ranks' rows (rank boundary * L not a
+    multiple of chunk) is refused on every rank (KS_ERR_SHARD), not summed in a
+    different order."""
+    res = run_world(2, _chunked_worker, 8, 2, 1024, 7, 3072, 1, [0, 4, 8])
+    assert isinstance(res[0], str) and isinstance(res[1], str)
+    assert "shard" in res[0].lower() or "13" in res[0]
