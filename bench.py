@@ -329,6 +329,9 @@ def run_ours(args, cfg_name, cfg):
 
     import paper_2604_25422_b200 as ks
 
+    for kv in args.opt:
+        name, val = kv.split("=")
+        ks.set_option(name, int(val))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -703,6 +706,7 @@ def run_ours(args, cfg_name, cfg):
                     "l2": "inputs larger than L2 (no flush)" if flush is None
                           else "L2 flushed before every timed step (512 MB write, untimed)",
                     "cuda_graphs": bool(graphs),
+                    **({"options": list(args.opt)} if args.opt else {}),
                     "step_timing": "one CUDA-graph replay per step (fwd + bwd)" if step_graph is not None
                                    else "per-path launches",
                     "step_bwd": "fused (ks_dwconv1d_bwd_f32)" if fused_bwd else "split (dx, dw calls)",
@@ -755,6 +759,8 @@ def main():
                     help="variant column of --timing-log (the reference's parser accepts naive/gmc/shared/warp)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-graphs", action="store_true", help="launch each path eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--opt", action="append", default=[],
+                    help="library tuning option name=value (ks_set_option; A/B runs, recorded in the line)")
     ap.add_argument("--bwd", choices=["fused", "split"], default="fused",
                     help="step backward: one ks_dwconv1d_bwd_f32 call (dX + dW in one pass) or the two calls")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -152,7 +152,7 @@ ks_status ks_launch_count(uint64_t* count);
  * reference); the determinism promise above is for the defaults.  Names:
  * disable_tma, ldg, sts, bwds, dst, dwtma_j16, dwtma_ns, pad_skip, pad_ns,
  * pad_prod, dwpad_ns, stencil_pad, stencil_r, stencil_nt, stencil_ns,
- * host_block_mb, stencil_bl, dw_ctas, dw_mrow, dwpad_min_k, sts_rows.  KS_OPTION_DEFAULT restores an option's default. */
+ * host_block_mb, stencil_bl, dw_ctas, dw_mrow, dwpad_min_k, sts_rows, pdl.  KS_OPTION_DEFAULT restores an option's default. */
 #define KS_OPTION_DEFAULT INT64_MIN
 ks_status ks_set_option(const char* name, int64_t value);
 ks_status ks_get_option(const char* name, int64_t* value);

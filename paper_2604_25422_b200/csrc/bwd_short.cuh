@@ -363,6 +363,7 @@ __global__ void __launch_bounds__(kThreads, Geo<KT, MODE>::MinBlocks)  // 3 CTAs
 bwd_short(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap x_map,
           const __grid_constant__ CUtensorMap out_map, const float* __restrict__ k, float* __restrict__ part, int B,
           int H, int L, int G, float* __restrict__ out, int rpi) {
+    pdl_wait();  // launched with PDL (the stencils follow prep_taps): predecessor complete first
     using Gm = Geo<KT, MODE>;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);

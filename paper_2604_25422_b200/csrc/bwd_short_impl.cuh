@@ -31,7 +31,7 @@ ks_status launch_k(const CUtensorMap& im, const CUtensorMap& xm, const CUtensorM
     const bool per_row = rows_opt == 1 || (rows_opt < 0 && FUSED && L >= 2 * kTT);
     const int64_t blocks = (MODE & 7) <= kFUSED ? int64_t(G) * H
                            : per_row ? B * H : std::min<int64_t>(B * H, int64_t(num_sms()) * per_sm);
-    launch_kernel(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
+    launch_kernel_pdl(kern, static_cast<unsigned>(blocks), kThreads, smem, st, im, xm, om, k, part, static_cast<int>(B),
                                                                 static_cast<int>(H), static_cast<int>(L), G, out, rpi);
     return check_launch();
 }

@@ -198,6 +198,7 @@ dw_hier_stage1(const float* __restrict__ gy, const float* __restrict__ x,
 // dk[h,j] = fixed-order sum over the G row-group partials.
 template <typename T>
 __global__ void dw_sum_groups(const T* __restrict__ part, T* __restrict__ dk, int64_t HK, int G) {
+    pdl_wait();  // launched with PDL after stage 1
     const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
     if (i >= HK) return;
     // ascending g, plain adds; the loads of a block of 8 groups are issued
@@ -608,7 +609,7 @@ ks_status dw_f32(const float* gy, const float* x, float* dk, int64_t B, int64_t 
     ks_status s = dw_stage1_only(gy, x, part, B, H, L, K, mode, 0, &G, st);
     if (s != KS_OK) return s;
     const int64_t HK = H * K;
-    launch_kernel(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, G);
+    launch_kernel_pdl(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, G);
     return check_launch();
 }
 
@@ -678,7 +679,7 @@ ks_status bwd_fused_f32(const float* gy, const float* x, const float* k, float* 
     const ks_status s = bwd_tma_stage1(gy, x, k, dx, part, B, H, L, K, pl.g, mode, st, fused);
     if (s != KS_OK || !*fused) return s;
     const int64_t HK = H * K;
-    launch_kernel(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, pl.g);
+    launch_kernel_pdl(dw_sum_groups<float>, static_cast<unsigned>((HK + 255) / 256), 256, 0, st, part, dk, HK, pl.g);
     return check_launch();
 }
 

@@ -121,6 +121,7 @@ bool encode_row_view_padded(CUtensorMap* map, const float* base, int64_t rows, i
 // reference's k[h, K-1-j] of src/conv_core.cpp:68), zero padded to Kp.
 __global__ void prep_taps(const float* __restrict__ k, float* __restrict__ kp, int64_t H, int64_t K, int64_t Kp,
                           int reverse, int lead) {
+    pdl_trigger();  // the stencil that reads kp may launch now (it waits for this grid)
     const int64_t n = H * Kp;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {

@@ -82,6 +82,38 @@ inline void launch_kernel(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t 
     if (note_launch(reinterpret_cast<const void*>(kern), grid, block, smem))
         kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
 }
+// Programmatic dependent launch (sm_90+): a kernel launched through
+// launch_kernel_pdl may start while its stream predecessor is still running;
+// it must call pdl_wait() before touching global memory (the wait returns once
+// the predecessor has completed and its writes are visible; without PDL it is
+// a no-op).  prep_taps triggers its dependents as it starts.  Option `pdl`.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+int64_t opt_pdl();
+template <typename... KArgs, typename... Args>
+inline void launch_kernel_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+    if (!note_launch(reinterpret_cast<const void*>(kern), grid, block, smem)) return;
+    // auto (-1): only small grids, where the launch gap is a visible share of
+    // the kernel (config 1 step -3..-5%; the large configs measured within noise)
+    const int64_t o = opt_pdl();
+    const bool use = o > 0 || (o < 0 && int64_t(grid.x) * grid.y * grid.z <= 1024);
+    if (!use) {
+        kern<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 // True while the calling thread is planning: no device work may be issued
 // (kernels are recorded by launch_kernel(); copies must be skipped by the caller).
 bool planning();
@@ -110,6 +142,7 @@ enum Opt {
     kOptDwMrow,
     kOptDwpadMinK,
     kOptStsRows,
+    kOptPdl,
     kOptCount
 };
 int64_t opt(Opt o);

@@ -47,6 +47,7 @@ constexpr OptDef kDefs[kOptCount] = {
     {"dw_mrow", 1, 0, 1},
     {"dwpad_min_k", 48, 17, 8192},   // smallest K whose dW takes dw_pad (below: dw_tma)        // K <= 16 dW with L < 2048: items of whole rows (0: one 2048-wide tile per row)
     {"sts_rows", -1, -1, 1},     // bwd_short stencils: one CTA per row (1), persistent grid (0), -1 auto (rows in Fused mode)  // HIERARCHICAL stage 1 (dw_tma / bwd_short / dw_rows / generic): target CTAs (sets G)
+    {"pdl", -1, -1, 1},          // programmatic dependent launch of the kernels after prep_taps / stage 1: 1 on, 0 off, -1 small grids
 };
 
 std::atomic<int64_t> g_opts[kOptCount];
@@ -78,6 +79,8 @@ int find(const char* name) {
 }
 
 }  // namespace
+
+int64_t opt_pdl() { return opt(kOptPdl); }
 
 int64_t opt(Opt o) {
     std::call_once(g_once, init_opts);

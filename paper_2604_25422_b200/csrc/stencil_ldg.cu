@@ -47,6 +47,7 @@ template <int KT, bool FUSED, bool REV, bool V8, bool MRW>
 __global__ void __launch_bounds__(256)
 stencil_ldg(const float* __restrict__ in, const float4* __restrict__ kp, float* __restrict__ out, int tpr, int H,
             int L, int rows, int rpc, int tprow) {
+    pdl_wait();  // launched with PDL after prep_taps: kp must be complete
     constexpr int OFF = REV ? KT - 1 - KT / 2 : KT / 2;
     constexpr int S = (4 - OFF % 4) % 4;              // window starts S floats into its first quad
     constexpr int NV = (S + 8 + KT - 1 + 3) / 4;      // quads per window
@@ -115,7 +116,7 @@ ks_status launch_k(bool fused, const float* in, const float4* kp, float* out, in
     const int h = static_cast<int>(H), l = static_cast<int>(L), nr = static_cast<int>(rows);
     const bool v8 = L % 8 == 0 && (reinterpret_cast<uintptr_t>(out) & 31) == 0;
 #define KS_LDG_LAUNCH(F, V, M) \
-    launch_kernel(stencil_ldg<KT, F, REV, V, M>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow)
+    launch_kernel_pdl(stencil_ldg<KT, F, REV, V, M>, grid, 256, 0, st, in, kp, out, tpr, h, l, nr, rpc, tprow)
     if (rpc > 1) {
         if (v8) { if (fused) KS_LDG_LAUNCH(true, true, true); else KS_LDG_LAUNCH(false, true, true); }
         else { if (fused) KS_LDG_LAUNCH(true, false, true); else KS_LDG_LAUNCH(false, false, true); }

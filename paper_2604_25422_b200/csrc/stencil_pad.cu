@@ -77,6 +77,7 @@ __global__ void prep_taps(const float*, float*, int64_t, int64_t, int64_t, int, 
 // padded layout), Kpp = Kp / 32 * 36 floats per row.
 __global__ void prep_taps_pad36(const float* __restrict__ k, float* __restrict__ kp, int64_t H, int64_t K,
                                 int64_t Kpp, int reverse, int lead) {
+    pdl_trigger();  // the stencil that reads kp may launch now (it waits for this grid)
     const int64_t n = H * Kpp;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -243,6 +244,7 @@ template <int S, bool FUSED, bool PROD, bool LANEB>
 __global__ void __launch_bounds__(kNT + (PROD ? 32 : 0))
 stencil_pad(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out,
             int H, int L, int tiles_per_row, int ntiles, PadGeom g, int NS) {
+    pdl_wait();  // launched with PDL after prep_taps: kp must be complete
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = align_smem<1024>(smem_raw);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * g.stage_bytes);
@@ -404,6 +406,7 @@ template <int S, bool FUSED>
 __global__ void __launch_bounds__(kNT + 32)
 stencil_bl(const __grid_constant__ CUtensorMap in_map, const float* __restrict__ kp, float* __restrict__ out, int B,
            int H, int L, BlGeom g) {
+    pdl_wait();  // launched with PDL after prep_taps: kp must be complete
     constexpr int NV = (S + kR + kJS - 1 + 3) / 4;
     constexpr int XP = S >= 2 ? 2 : 1;  // pieces past Q a block reads
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -546,7 +549,7 @@ ks_status launch_bl(const CUtensorMap& im, const float* kp, float* out, int64_t 
     auto kern = stencil_bl<S, FUSED>;
     const int smem = bl_smem(g);
     prepare_kernel(reinterpret_cast<const void*>(kern), kNT + 32, smem);
-    launch_kernel(kern, static_cast<unsigned>(int64_t(g.ncol) * g.ngrp * H), kNT + 32, smem, st, im, kp, out,
+    launch_kernel_pdl(kern, static_cast<unsigned>(int64_t(g.ncol) * g.ngrp * H), kNT + 32, smem, st, im, kp, out,
                   static_cast<int>(B), static_cast<int>(H), static_cast<int>(L), g);
     return check_launch();
 }
@@ -564,7 +567,7 @@ ks_status launch(const CUtensorMap& im, const float* kp, float* out, int64_t B, 
     const int tiles_per_row = static_cast<int>((L + T - 1) / T);
     const int ntiles = static_cast<int>(B * H / g.RPT * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
-    launch_kernel(kern, grid, threads, smem, st, im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
+    launch_kernel_pdl(kern, grid, threads, smem, st, im, kp, out, static_cast<int>(H), static_cast<int>(L), tiles_per_row, ntiles,
                                       g, NS);
     return check_launch();
 }

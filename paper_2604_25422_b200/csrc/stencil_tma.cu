@@ -67,6 +67,7 @@ __global__ void __launch_bounds__(NT)
 stencil_tma(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
             const float* __restrict__ kp, float* __restrict__ out, int H, int L, int K, int tiles_per_row,
             int ntiles, StencilGeom g, int NS) {
+    pdl_wait();  // launched with PDL after prep_taps: kp must be complete
     constexpr int SW = R == 4 ? 0 : 128;
     constexpr int NV = (S + R + kJB - 1 + 3) / 4;
     extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -196,7 +197,7 @@ ks_status launch(const CUtensorMap& im, const CUtensorMap& om, const float* kp, 
     const int tiles_per_row = static_cast<int>((L + g.T - 1) / g.T);
     const int ntiles = static_cast<int>(B * H * tiles_per_row);
     const int grid = std::min(ntiles, num_sms() * per_sm);
-    launch_kernel(kern, grid, NT, smem, st, im, om, kp, out, static_cast<int>(H), static_cast<int>(L), static_cast<int>(K),
+    launch_kernel_pdl(kern, grid, NT, smem, st, im, om, kp, out, static_cast<int>(H), static_cast<int>(L), static_cast<int>(K),
                                  tiles_per_row, ntiles, g, NS);
     return check_launch();
 }
