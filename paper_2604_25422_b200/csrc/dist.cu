@@ -164,6 +164,10 @@ ks_status ks_dwconv1d_dw_chunked_sharded_f32(const float* gy, const float* x, fl
     }
     const int64_t HK = H * K;
     const size_t n = static_cast<size_t>(std::max<int64_t>(1, ncmax) * HK);
+    if (double(n) * world * sizeof(float) > double(size_t(4) << 30)) {  // the gathered partials of every rank
+        set_last_error("sharded CHUNKED dW: more than 4 GiB of chunk partials to gather (use a larger chunk)");
+        return KS_ERR_SHARD;
+    }
     float *part = nullptr, *gather = nullptr;
     s = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&part), n * sizeof(float), st));
     if (s == KS_OK) s = cuda_status(cudaMallocAsync(reinterpret_cast<void**>(&gather), n * world * sizeof(float), st));
