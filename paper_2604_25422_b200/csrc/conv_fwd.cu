@@ -179,12 +179,9 @@ template <int R, int S, bool FUSED>
 static ks_status launch_tile(const float* in, const float* k, float* out, int64_t B, int64_t H,
                              int64_t L, int64_t K, int64_t off, int reverse, cudaStream_t st) {
     const size_t smem = tile_smem_bytes<R, S, FUSED>(static_cast<int>(K));
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(conv_tile_f32<R, S, FUSED>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set = true;
-    }
+    // per device and thread-safe (a function-local flag would opt in only the
+    // first device a process uses)
+    prepare_kernel(reinterpret_cast<const void*>(conv_tile_f32<R, S, FUSED>), kTileThreads, static_cast<int>(smem));
     const int tiles = static_cast<int>((L + TileGeom<R>::T - 1) / TileGeom<R>::T);
     const int64_t blocks = B * H * tiles;
     launch_kernel(conv_tile_f32<R, S, FUSED>, static_cast<unsigned>(blocks), kTileThreads, smem, st, 

@@ -422,7 +422,8 @@ def test_stencil_short_equals_generic_and_oracle(K, oracle):
                                    (12, 3, 1024, 16), (9, 2, 1984, 13), (30, 3, 256, 16), (7, 5, 500, 7),
                                    (5, 3, 1000, 12), (3, 7, 4092, 5), (4, 3, 2052, 9), (5, 3, 1000, 16),
                                    (7, 5, 500, 14), (33, 3, 260, 5), (16, 5, 512, 20), (12, 4, 256, 27),
-                                   (9, 3, 992, 31), (11, 2, 500, 32)])
+                                   (9, 3, 992, 31), (11, 2, 500, 32), (5, 3, 4095, 7), (4, 3, 1023, 40),
+                                   (3, 5, 777, 100), (6, 2, 2049, 3), (2, 3, 4093, 1)])
 def test_mid_length_rows_register_tiles(oracle, shape):
     """Rows shorter than 2048 that the whole-row kernels (stencil_rows) do
     not take: stencil_tma's R = 4 tiles sized to the row (32..256 threads),

@@ -18,7 +18,8 @@ import paper_2604_25422_b200 as ks  # noqa: E402
 from oracle.oracle import CHUNKED, PAIRWISE, SEQUENTIAL, Oracle  # noqa: E402
 
 o = Oracle()
-shapes = [(2, 3, 4096, 7), (2, 2, 1024, 64), (1, 2, 2048, 256), (2, 2, 1000, 5), (1, 1, 96, 40)]
+shapes = [(2, 3, 4096, 7), (2, 2, 1024, 64), (1, 2, 2048, 256), (2, 2, 1000, 5), (1, 1, 96, 40),
+          (2, 3, 4095, 7), (1, 2, 1023, 40)]  # odd L: the generic kernels' shifted aligned loads
 for (B, H, L, K) in shapes:
     x, k, gy = o.fill_inputs(3, B, H, L, K)
     dx_, dk_, dgy = (torch.from_numpy(a).cuda() for a in (x, k, gy))
