@@ -133,10 +133,23 @@ ks_status ks_dwconv1d_dw_chunked_sharded_f32(const float* gy, const float* x, fl
     const int world = comm->world;
     // every rank's rows: they must tile [0, B_total) in rank order, and no
     // chunk may straddle two ranks (each chunk's chain is computed whole)
-    int64_t mine[2] = {b0, B_local};
-    std::vector<int64_t> all(2 * static_cast<size_t>(world));
-    ks_status s = comm_allgather_host(comm, mine, all.data(), sizeof(mine));
+    // every rank's rows, and the shape / chunk / mode every rank must agree on
+    // (a disagreement would make the gathers mismatch)
+    constexpr int kRec = 8;
+    int64_t mine[kRec] = {b0, B_local, B_total, H, L, K, chunk, mode};
+    std::vector<int64_t> rec(kRec * static_cast<size_t>(world));
+    ks_status s = comm_allgather_host(comm, mine, rec.data(), sizeof(mine));
     if (s != KS_OK) return s;
+    std::vector<int64_t> all(2 * static_cast<size_t>(world));
+    for (int r = 0; r < world; ++r) {
+        for (int f = 2; f < kRec; ++f)
+            if (rec[kRec * r + f] != mine[f]) {
+                set_last_error("sharded CHUNKED dW: ranks disagree on (B_total, H, L, K, chunk, mode)");
+                return KS_ERR_SHARD;
+            }
+        all[2 * r] = rec[kRec * r];
+        all[2 * r + 1] = rec[kRec * r + 1];
+    }
     const int64_t n_flat = B_total * L;
     const int64_t c_eff = std::min(chunk, n_flat);  // chunk >= B*L: one chunk (SEQUENTIAL)
     std::vector<int> counts(world);

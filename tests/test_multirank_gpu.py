@@ -253,3 +253,26 @@ def test_chunked_dw_sharded_rejects_straddling_chunks():
     res = run_world(2, _chunked_worker, 8, 2, 1024, 7, 3072, 1, [0, 4, 8])
     assert isinstance(res[0], str) and isinstance(res[1], str)
     assert "shard" in res[0].lower() or "13" in res[0]
+
+
+def _chunked_mismatch_worker(rank, world, results):
+    import paper_2604_25422_b200 as ks
+    torch.cuda.set_device(0)
+    comm = ks.Comm.host(world, rank, gloo_allgather)
+    try:
+        K = 7 if rank == 0 else 9  # the ranks disagree on K
+        x, k, gy = ks.make_inputs(7, 4, 2, 1024, K, device="cuda", b0=4 * rank, B_total=8)
+        try:
+            comm.chunked_dw(gy, x, K, 1024, ks.FUSED, 4 * rank, 8)
+            results[rank] = "ok"
+        except ks.KsError as e:
+            results[rank] = f"error: {e}"
+    finally:
+        comm.close()
+
+
+def test_chunked_dw_sharded_rejects_disagreeing_ranks():
+    """Ranks that disagree on the shape are refused on every rank before any
+    gather of differently sized partials."""
+    res = run_world(2, _chunked_mismatch_worker)
+    assert res[0].startswith("error") and res[1].startswith("error")
