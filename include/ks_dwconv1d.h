@@ -268,8 +268,9 @@ ks_status ks_dwconv1d_dw_allgather_sum_f32(float* dk, float* gather, int64_t H, 
  * spread over the ranks, so the bits do not depend on the number of GPUs
  * (SURVEY 8(e)'s G-invariant option).  Rank r holds global rows
  * [b0, b0 + B_local) of B_total; the ranks' rows must tile [0, B_total) in
- * rank order with every rank boundary (row * L) a multiple of `chunk`, else
- * KS_ERR_SHARD.  Each rank computes the partials of its own chunks, they are
+ * rank order with every rank boundary (row * L) a multiple of `chunk`, and
+ * all ranks must pass the same (B_total, H, L, K, chunk, mode); else
+ * KS_ERR_SHARD on every rank.  Each rank computes the partials of its own chunks, they are
  * all-gathered (rank order = global chunk order) and every rank adds them in
  * chunk order.  dk[H,K] is written on every rank.  Synchronous on a host
  * communicator; on an NCCL communicator the gather runs on `stream`. */
